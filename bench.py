@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: approximate-LUT ResNet inference on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload r8|r50|r62] [--impl b200|reference]
+
+A step = one range-batch of synthetic images through the whole transformed
+ResNet graph (every conv an AxConv2D with the approximate truth table, the
+classifier a 1x1 AxConv2D): range reduction, quantize + zp-pad, LUT implicit
+GEMM with fused correction/dequant/bias/residual/ReLU/next-range epilogue,
+pools.  Default workload = BASELINE.json configs[1]: ResNet-8 CIFAR-10,
+batch 1024 per GPU, truncated_lut(signed, 2).
+
+Data parallel by range-batch (ranges are per batch, graph.py:270-275): each
+rank runs its own batch with zero per-layer communication ("scaling": "weak");
+NCCL only all-gathers logits and all-reduces prediction counts after the
+timed region.  Timing: W warm-up steps, then K steps bracketed by barrier +
+synchronize; each step is timed with CUDA events on the launching stream and
+L2 is flushed (256 MiB write) between steps outside the events; the job
+time is the max over ranks.
+
+value = approximate GMAC/s of the whole job (algorithmic MACs as
+graph_mac_count, graph.py:316-349); images/s alongside.  e2e = the same
+metric through the public GpuGraph.run API from pinned HOST batches, H2D copy
+of the images and D2H copy of the logits inside the timed region.
+
+--impl reference: the reference's CPU algorithm (the pinned oracle port:
+numpy + C/OpenMP LUT-GEMM, all host threads) on a bounded sample of the same
+workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "approximate GMAC/s and images/s (ResNet, synthetic) at 1/2/4/8 B200 vs CPU ref"
+# paper-derived GTX 1080 approximate throughput for the same CIFAR nets
+PAPER_GMACS = {"r8": 140.0, "r62": 95.5}
+
+
+def workload_spec(name: str, lut_kind: str):
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200 import types as T
+
+    if lut_kind == "trunc2":
+        lut = T.truncated_lut(T.Signedness.SIGNED, 2)
+        lut_desc = "truncated_lut(signed, 2)"
+    elif lut_kind == "exact":
+        lut = T.exact_lut(T.Signedness.SIGNED)
+        lut_desc = "exact_lut(signed)"
+    else:
+        lut = T.random_lut(np.random.default_rng(123), T.Signedness.SIGNED)
+        lut_desc = "random_lut(signed, seed 123)"
+    if name == "r8":
+        return dict(nodes=resnet.cifar_resnet(1, lut, seed=0), batch=1024, kind="cifar", lut=lut_desc,
+                    desc="ResNet-8 CIFAR-10 (He 6n+2, n=1; 9 convs + 1x1 AxConv2D classifier)")
+    if name == "r62":
+        return dict(nodes=resnet.cifar_resnet(10, lut, seed=0), batch=1000, kind="cifar", lut=lut_desc,
+                    desc="ResNet-62 CIFAR-10 (He 6n+2, n=10; 63 convs + 1x1 AxConv2D classifier)")
+    if name == "r50":
+        return dict(nodes=resnet.resnet50(lut, seed=0), batch=256, kind="imagenet", lut=lut_desc,
+                    desc="ResNet-50 v1.5 224x224 (53 convs + 1x1 AxConv2D classifier), BN folded")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def make_images(kind: str, n: int, seed: int):
+    from paper_2002_09481_b200 import datasets
+
+    if kind == "cifar":
+        return datasets.synthetic_cifar10(n, seed=seed)
+    return datasets.uniform_images(n, 224, seed=seed), np.zeros(n, np.uint8)
+
+
+# ---------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if not self.lines:  # timed region shorter than one sampling period: take one sample now
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                self.lines.extend(out.stdout.strip().splitlines())
+            except Exception:
+                pass
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- CPU baseline
+
+
+def oracle_nodes(nodes):
+    out = []
+    for n in nodes:
+        a = dict(n["attrs"])
+        if "lut" in a:
+            a["mode"], a["lut"] = a["lut"].mode.value, a["lut"].entries
+        out.append({"id": n["id"], "kind": n["kind"], "inputs": n["inputs"], "attrs": a})
+    return out
+
+
+def cpu_reference_rate(spec, macs_per_img: int, budget_s: float, seed: int = 0):
+    """Time the oracle port (reference algorithm, all host threads) on a bounded sample."""
+    from oracle import axemu_oracle as O
+
+    onodes = oracle_nodes(spec["nodes"])
+    n = 2 if spec["kind"] == "imagenet" else 16
+    x, _ = make_images(spec["kind"], n, seed)
+    O.run_graph(onodes, x[:1])  # warm-up (page-in, OpenMP pool)
+    t0 = time.perf_counter()
+    O.run_graph(onodes, x)
+    dt = time.perf_counter() - t0
+    # scale the sample towards the time budget (bounded)
+    scale = max(1, min(int(budget_s / max(dt, 1e-3)), 64 if spec["kind"] == "cifar" else 8))
+    if scale > 1:
+        n2 = n * scale
+        x, _ = make_images(spec["kind"], n2, seed)
+        t0 = time.perf_counter()
+        O.run_graph(onodes, x)
+        dt = time.perf_counter() - t0
+        n = n2
+    gmacs = n * macs_per_img / dt / 1e9
+    return dict(value=round(gmacs, 4), unit="GMAC/s", images_per_s=round(n / dt, 3), cores=O.threads(),
+                kind="port", sample=f"{n} images of the same workload through the oracle port "
+                                    f"(numpy + C/OpenMP int64 LUT-GEMM), {dt:.2f} s")
+
+
+# ---------------------------------------------------------------------------- main
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="r8", choices=["r8", "r50", "r62"])
+    ap.add_argument("--lut", default="trunc2", choices=["trunc2", "exact", "random"])
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers-out", default="")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    spec = workload_spec(args.workload, args.lut)
+    batch = args.batch or spec["batch"]
+    from paper_2002_09481_b200 import resnet
+
+    macs_img = resnet.macs_per_image(spec["nodes"])
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = []
+        for _ in range(args.warmup):
+            pass
+        info = None
+        for k in range(max(1, args.steps)):
+            info = cpu_reference_rate(spec, macs_img, budget_s=min(args.cpu_budget, 20.0), seed=k)
+            steps.append(info["value"])
+        val = statistics.median(steps)
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GMAC/s",
+                "images_per_s": round(val * 1e9 / macs_img, 3), "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "u8", "data": "synthetic",
+                "config": {"workload": spec["desc"], "batch_per_gpu": batch, "lut": spec["lut"]},
+                "cpu_baseline": {"value": val, "unit": "GMAC/s", "cores": info["cores"], "kind": "port",
+                                 "sample": info["sample"]},
+                "e2e": {"value": val, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    graph = GpuGraph(spec["nodes"], device=local)
+    imgs, labels = make_images(spec["kind"], batch, seed=1000 + rank)
+    x_dev = torch.from_numpy(imgs).to(dev)
+    x_host = torch.from_numpy(imgs).pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # warm-up (also prepares filters once: hoisted quantize_filters)
+    for _ in range(args.warmup):
+        y = graph.run(x_dev, check=True)
+    torch.cuda.synchronize()
+    launches = graph.launches
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------ device-resident timed region
+    sampler = ClockSampler(local)
+    sampler.start()
+    profile: list = []
+    barrier()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()  # write > L2 (126 MB) between timed steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        y = graph.run(x_dev, check=False, profile=profile)
+        e1.record()
+        step_ms.append((e0, e1))
+    barrier()
+    clocks = sampler.stop()
+    per_step = [a.elapsed_time(b) for a, b in step_ms]
+    total_ms = sum(per_step)
+    conv_ms = sum(a.elapsed_time(b) for _, a, b, _ in profile)
+    conv_macs = sum(m for *_, m in profile)
+    layer_rows = {}
+    for nid, a, b, m in profile:
+        r = layer_rows.setdefault(nid, [0.0, 0, 0])
+        r[0] += a.elapsed_time(b)
+        r[1] += m
+        r[2] += 1
+    graph.check_flags()
+
+    # ------------------------------------------------ end-to-end through the public API (host buffers)
+    out_host = torch.empty(tuple(y.shape), dtype=torch.float32).pin_memory()
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        xd = x_host.to(dev, non_blocking=True)
+        yd = graph.run(xd, check=False)
+        out_host.copy_(yd, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    barrier()
+    e2e_total = sum(e2e_ms)
+
+    # ------------------------------------------------ max over ranks, NCCL gather of logits/counts
+    from paper_2002_09481_b200.dist import exchange_results
+
+    t = torch.tensor([total_ms, e2e_total, conv_ms], dtype=torch.float64, device=dev)
+    logits = y.reshape(batch, -1)
+    pred = logits.argmax(1)
+    agree = (pred.cpu().numpy() == labels.astype(np.int64)).sum()
+    cnt = torch.tensor([int(agree), batch], dtype=torch.int64, device=dev)
+    gathered, cnt, t = exchange_results(logits, cnt, t)
+    total_ms, e2e_total, conv_ms_max = (float(v) for v in t.tolist())
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    images = batch * world * args.steps
+    gmacs = images * macs_img / (total_ms / 1e3) / 1e9
+    e2e_gmacs = images * macs_img / (e2e_total / 1e3) / 1e9
+
+    import json as _json
+
+    peaks = {}
+    try:
+        peaks = _json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    max_mhz = float(peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0)
+    peak_lookups = sm_count * 32 * max_mhz * 1e6  # one 32-lane LDS wavefront per SM per clock
+    achieved = conv_macs / (conv_ms / 1e3) if conv_ms else 0.0
+    sampled = clocks.get("sm_mhz")
+    roofline = {
+        "bound": "smem", "kernel": "lutconv_fast (LUT implicit GEMM, all conv launches of a step)",
+        "achieved": round(achieved / 1e9, 2), "peak": round(peak_lookups / 1e9, 2), "unit": "Glookup/s",
+        "frac": round(achieved / peak_lookups, 4),
+        "frac_at_sampled_clock": round(achieved / (sm_count * 32 * sampled * 1e6), 4) if sampled else None,
+        "peak_basis": f"derived: {sm_count} SMs x 32 lookups/clk x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+        "traffic": None, "conv_share_of_step": round(conv_ms / total_ms, 4) if total_ms else None,
+    }
+    line = {
+        "metric": METRIC, "value": round(gmacs, 2), "unit": "GMAC/s",
+        "images_per_s": round(images / (total_ms / 1e3), 2), "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": round(gmacs / PAPER_GMACS[args.workload], 2) if args.workload in PAPER_GMACS else None,
+        "vs_baseline_basis": "paper-derived GTX 1080 approx GMAC/s (BASELINE.md s1)" if args.workload in PAPER_GMACS else None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {"workload": spec["desc"], "batch_per_gpu": batch, "lut": spec["lut"],
+                   "macs_per_image": macs_img, "parallelism": f"dp{world} (one range-batch per GPU)",
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+        "roofline": roofline,
+        "e2e": {"value": round(e2e_gmacs, 2), "unit": "GMAC/s", "images_per_s": round(images / (e2e_total / 1e3), 2),
+                "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4)},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+        "agreement_with_labels": round(float(cnt[0]) / float(cnt[1]), 4),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_reference_rate(spec, macs_img, budget_s=args.cpu_budget)
+    if args.layers_out:
+        rows = [{"node": k, "ms": round(v[0] / v[2], 4), "gmacs": round(v[1] / (v[0] / 1e3) / 1e9, 1),
+                 "frac": round(v[1] / (v[0] / 1e3) / peak_lookups, 4)} for k, v in layer_rows.items()]
+        Path(args.layers_out).write_text(json.dumps(rows, indent=1))
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

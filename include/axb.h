@@ -1,0 +1,159 @@
+/*
+ * axb.h -- C ABI of the B200-native approximate-convolution path
+ * (paper_2002_09481_b200, "axb").  Plain pointers and sizes only; every
+ * pointer named d_* or documented "device" is CUDA device memory owned by
+ * the caller.  All launches are stream-ordered on the given cudaStream_t
+ * (passed as void*); no function synchronises unless documented.
+ *
+ * Return value: 0 = OK, otherwise one of AXB_E_*; axb_last_error() gives the
+ * message (thread-local).  The Python adapter maps codes back to the
+ * reference's exception types (ValueError / OverflowError).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/axemu):
+ *   axb_lut_create          <- axmult.py:22-43    MultLut (table, index (a<<8)|b)
+ *   axb_range_reset/minmax  <- tensor.py:143-149  tensor_min_max; graph.py:270-275 Min/Max nodes
+ *   axb_coeffs_from_range   <- quantizer.py:98-117 compute_coeffs (device-side, no host sync)
+ *   axb_coeffs_host         <- quantizer.py:98-117 compute_coeffs (host scalars)
+ *   axb_quantize_pad        <- quantizer.py:120-131 quantize_values + axconv.py:181-189 zp padding
+ *   axb_filters_prepare     <- axconv.py:199-210  quantize_filters (K x Cout codes + S_f)
+ *   axb_conv2d_lut          <- axconv.py:213-257  approx_gemm/_lut_matmul (:136-146) + im2cols
+ *                              (:160-196, implicit) + graph.py:268-277 bias / ReLU epilogue
+ *   axb_axconv2d            <- axconv.py:266-297  axconv2d (whole operator, one call)
+ *   axb_maxpool/avgpool     <- graph.py:182-199   _pool2d (float glue around the op)
+ *   axb_add_relu            <- graph.py:276-286   ReLU / Add nodes
+ */
+#ifndef AXB_H
+#define AXB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AXB_OK 0
+#define AXB_E_VALUE 1     /* -> ValueError    (shapes, layouts, non-finite, bad params) */
+#define AXB_E_OVERFLOW 2  /* -> OverflowError (32-bit code-sum overflow)              */
+#define AXB_E_CUDA 3      /* -> RuntimeError  (CUDA launch / allocation failure)       */
+
+/* flag bits written by kernels into a device int32 (checked by the host) */
+#define AXB_FLAG_NONFINITE 1      /* non-finite value to quantize / in a range (ValueError) */
+#define AXB_FLAG_PSUM_OVF 2       /* patch code sum outside int32 (OverflowError)           */
+#define AXB_FLAG_OUT_NONFINITE 4  /* non-finite kernel output feeding a fused range         */
+#define AXB_FLAG_FSUM_OVF 8       /* filter code sum outside int32 (OverflowError)          */
+
+/* signedness / rounding / accumulator enums (quantizer.py:28-49, axconv.py:47-58) */
+#define AXB_UNSIGNED 0
+#define AXB_SIGNED 1
+#define AXB_ROUND_HALF_AWAY 0
+#define AXB_ROUND_HALF_EVEN 1
+#define AXB_ROUND_TOWARD_ZERO 2
+#define AXB_ACC_EXACT64 0
+#define AXB_ACC_WRAP32 1
+#define AXB_ACC_SATURATE32 2
+
+/* QuantParams (quantizer.py:60-74); lives in device memory for the kernels */
+typedef struct axb_qparams {
+    double scale;
+    int32_t zero_point;
+    int32_t valid; /* 1 once computed */
+} axb_qparams;
+
+typedef struct axb_lut axb_lut; /* opaque: device copies of one truth table */
+
+const char *axb_last_error(void);
+int axb_version(void);
+int axb_device_info(int device, int *sm_count, int *smem_optin_bytes, int *cc_major, int *cc_minor);
+
+/* ---- multiplier table ---------------------------------------------------- */
+/* entries: 65,536 raw 16-bit words, host memory, index (a_byte << 8) | b_byte
+ * (a = activation / first operand, b = filter / second operand). */
+int axb_lut_create(const uint16_t *entries, int is_signed, axb_lut **out);
+int axb_lut_destroy(axb_lut *lut);
+int axb_lut_is_signed(const axb_lut *lut);
+/* device pointer of the b-major (transposed) copy used by the conv kernels */
+const uint16_t *axb_lut_device_bmajor(const axb_lut *lut);
+
+/* ---- K1: range reduction ------------------------------------------------- */
+/* d_range: 2 x int32 ordered-float accumulators [min, max]; reset sets +inf/-inf */
+int axb_range_reset(int32_t *d_range, void *stream);
+int axb_range_minmax(const float *d_x, int64_t n, int32_t *d_range, int32_t *d_flags, void *stream);
+/* read back (synchronises): min/max as float, nonfinite flag */
+int axb_range_read(const int32_t *d_range, const int32_t *d_flags, float *mn, float *mx, int32_t *flags,
+                   void *stream);
+
+/* ---- coefficients -------------------------------------------------------- */
+int axb_coeffs_host(double mn, double mx, int is_signed, int round_mode, axb_qparams *out);
+int axb_coeffs_from_range(const int32_t *d_range, int is_signed, int round_mode, axb_qparams *d_out,
+                          void *stream);
+int axb_params_upload(const axb_qparams *host_params, axb_qparams *d_params, void *stream);
+
+/* ---- K2: quantize into a zero-point-padded uint8 NHWC tensor -------------- */
+/* d_x: (n,h,w,c) fp32; d_codes: (n, h+pt+pb, w+pl+pr, cs) raw code bytes with
+ * the border = zero-point code and channels c..cs-1 = 0; d_pixsum: per padded
+ * pixel sum of the c code values (int32).  cs = axb_channel_stride(c). */
+int64_t axb_channel_stride(int64_t c);
+int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
+                     int32_t pl, int32_t pr, int64_t cs, const axb_qparams *d_params, int is_signed,
+                     int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags, void *stream);
+
+/* ---- filter preparation (once per layer) ---------------------------------- */
+/* d_f: HWCN fp32 (kh,kw,c,cout).  d_fcodes: (kpad, coutp) uint16 = 2*raw code
+ * (row k = (ky*kw + kx)*cs + ci; junk rows / columns = 0); d_fsum: int64[cout]. */
+int64_t axb_filter_kpad(int64_t kh, int64_t kw, int64_t cs);
+int64_t axb_filter_coutp(int64_t cout);
+int axb_filters_prepare(const float *d_f, int64_t kh, int64_t kw, int64_t c, int64_t cout, int64_t cs,
+                        const axb_qparams *d_params, int is_signed, int round_mode, uint16_t *d_fcodes,
+                        int64_t *d_fsum, int32_t *d_flags, void *stream);
+
+/* ---- K3: LUT implicit-GEMM convolution with fused epilogue ---------------- */
+typedef struct axb_conv_desc {
+    const uint8_t *codes;   /* zp-padded input codes (n, hp, wp, cs)               */
+    const int32_t *pixsum;  /* (n, hp, wp) code sums                                */
+    int64_t n, hp, wp, cs, c;
+    int32_t kh, kw, sh, sw, dh, dw;
+    int64_t oh, ow;
+    const uint16_t *fcodes; /* (kpad, coutp) from axb_filters_prepare               */
+    const int64_t *fsum;    /* (cout)                                               */
+    int64_t cout, coutp, kpad;
+    const axb_qparams *in_params; /* device */
+    const axb_qparams *f_params;  /* device */
+    int32_t accumulator;    /* AXB_ACC_*                                            */
+    int32_t relu;           /* 1: max(y, 0) after bias/residual (graph.py:276-277)  */
+    const float *bias;      /* nullable, fp32[cout] (graph.py:268-269)              */
+    const float *residual;  /* nullable, fp32 (n,oh,ow,cout) added after bias       */
+    float *out;             /* fp32 (n, oh, ow, cout)                               */
+    int64_t *acc_out;       /* nullable: emulated raw LUT sums A (int64)            */
+    int32_t *out_range;     /* nullable: ordered-float [min,max] of out (next layer) */
+    int32_t *flags;         /* device int32 flag word                               */
+    int32_t force_generic;  /* 1: use the int64 generic kernel (testing)            */
+    int32_t sm_limit;       /* 0 = all SMs; else cap persistent grid                 */
+} axb_conv_desc;
+
+int axb_conv2d_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);
+/* which kernel variant the last axb_conv2d_lut call on this thread launched */
+const char *axb_last_kernel(void);
+
+/* ---- whole operator (axconv2d) on device buffers, host ranges ------------- */
+/* pads: resolved (top,bottom,left,right).  Synchronises once to check flags. */
+int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, const float *d_f, int64_t kh,
+                 int64_t kw, int64_t cout, int32_t sh, int32_t sw, int32_t dh, int32_t dw, int32_t pt,
+                 int32_t pb, int32_t pl, int32_t pr, double in_min, double in_max, double f_min,
+                 double f_max, int32_t round_mode, int32_t accumulator, const axb_lut *lut, float *d_out,
+                 int64_t *d_acc_out, void *stream);
+
+/* ---- float glue for the graph executor ------------------------------------ */
+int axb_maxpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t ph, int32_t pw,
+                int32_t sh, int32_t sw, int32_t pt, int32_t pl, int64_t oh, int64_t ow, float *d_out,
+                int32_t *d_out_range, int32_t *d_flags, void *stream);
+int axb_avgpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t ph, int32_t pw,
+                int32_t sh, int32_t sw, int32_t pt, int32_t pl, int64_t oh, int64_t ow, float *d_out,
+                int32_t *d_out_range, int32_t *d_flags, void *stream);
+/* out = relu?(a + b?) elementwise fp32; b nullable */
+int axb_add_relu(const float *d_a, const float *d_b, int64_t n, int32_t relu, float *d_out, int32_t *d_out_range,
+                 int32_t *d_flags, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AXB_H */

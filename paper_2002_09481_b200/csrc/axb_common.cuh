@@ -1,0 +1,105 @@
+// Shared device helpers for the axb kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "axb.h"
+
+namespace axb {
+
+constexpr int kLutEntries = 65536;
+constexpr int kLutBytes = kLutEntries * 2;  // 128 KiB
+
+// ---- ordered-float <-> int (monotone map so atomicMin/Max on int == float min/max)
+__host__ __device__ __forceinline__ int32_t f2ord(float f) {
+#ifdef __CUDA_ARCH__
+    int32_t i = __float_as_int(f);
+#else
+    int32_t i;
+    memcpy(&i, &f, 4);
+#endif
+    return i >= 0 ? i : (i ^ 0x7FFFFFFF);
+}
+__host__ __device__ __forceinline__ float ord2f(int32_t i) {
+    int32_t b = i >= 0 ? i : (i ^ 0x7FFFFFFF);
+#ifdef __CUDA_ARCH__
+    return __int_as_float(b);
+#else
+    float f;
+    memcpy(&f, &b, 4);
+    return f;
+#endif
+}
+
+// ---- compute_coeffs (quantizer.py:98-117), identical IEEE fp64 op sequence
+__host__ __device__ inline double apply_round(double x, int mode) {
+    if (mode == AXB_ROUND_HALF_AWAY) return copysign(floor(fabs(x) + 0.5), x);  // :52-53
+    if (mode == AXB_ROUND_HALF_EVEN) return rint(x);                            // :54-55
+    return trunc(x);                                                            // :56
+}
+
+__host__ __device__ inline axb_qparams coeffs(double mn, double mx, int is_signed, int round_mode) {
+    mn = (0.0 < mn) ? 0.0 : mn;  // Python min(rng.min, 0.0): first arg unless 0.0 < it
+    mx = (0.0 > mx) ? 0.0 : mx;  // Python max(rng.max, 0.0): first arg unless 0.0 > it
+    double scale = (mx - mn) / 255.0;
+    if (scale == 0.0) scale = 1.0;
+    const double lo = is_signed ? -128.0 : 0.0, hi = is_signed ? 127.0 : 255.0;
+    double zp_real = lo - mn / scale;
+    double r = apply_round(zp_real, round_mode);
+    r = r < lo ? lo : (r > hi ? hi : r);  // np.clip
+    axb_qparams p;
+    p.scale = scale;
+    p.zero_point = (int32_t)r;
+    p.valid = 1;
+    return p;
+}
+
+// ---- quantize_values (quantizer.py:120-131) for one element; returns the code value
+__device__ __forceinline__ int quantize_one(float v, double scale, int zp, int is_signed, int round_mode) {
+    const double x = (double)v / scale;  // IEEE div.rn.f64
+    const double nearest = rint(x);
+    const double ax = fabs(x);
+    const bool snapped = fabs(x - nearest) <= 1.52587890625e-05 * (ax > 1.0 ? ax : 1.0);  // 2^-16
+    double r;
+    if (snapped)
+        r = nearest;
+    else if (round_mode == AXB_ROUND_HALF_AWAY)
+        r = copysign(floor(ax + 0.5), x);
+    else if (round_mode == AXB_ROUND_HALF_EVEN)
+        r = nearest;
+    else
+        r = trunc(x);
+    const double lo = is_signed ? -128.0 : 0.0, hi = is_signed ? 127.0 : 255.0;
+    double c = r + (double)zp;
+    c = c < lo ? lo : (c > hi ? hi : c);
+    return (int)c;
+}
+
+// ---- warp reductions
+__device__ __forceinline__ int32_t warp_min_i(int32_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int32_t warp_max_i(int32_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-level range accumulation of a thread's running [min,max] (ordered ints) + nonfinite.
+__device__ __forceinline__ void range_commit(int32_t tmin, int32_t tmax, int nonfinite, int32_t *d_range,
+                                             int32_t *d_flags, int32_t flag_bit) {
+    tmin = warp_min_i(tmin);
+    tmax = warp_max_i(tmax);
+    const unsigned nf = __ballot_sync(0xffffffffu, nonfinite);
+    if ((threadIdx.x & 31) == 0) {
+        if (d_range) {
+            if (tmin != INT32_MAX) atomicMin(d_range, tmin);
+            if (tmax != INT32_MIN) atomicMax(d_range + 1, tmax);
+        }
+        if (nf && d_flags) atomicOr(d_flags, flag_bit);
+    }
+}
+
+}  // namespace axb

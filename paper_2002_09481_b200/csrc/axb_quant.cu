@@ -1,0 +1,343 @@
+// K1 (range reduction), coefficients, K2 (quantize + zero-point padding) and
+// filter preparation.  All HBM-bound; bit-exact restatements of
+//   tensor.py:143-149 / graph.py:270-275 (min/max, non-finite -> ValueError)
+//   quantizer.py:98-117 (compute_coeffs), :120-131 (quantize_values)
+//   axconv.py:181-196 (zp padding, patch sums), :199-210 (quantize_filters)
+#include "axb_common.cuh"
+#include "axb_internal.h"
+
+namespace axb {
+
+// ---------------------------------------------------------------- K1: range
+// Grid-stride over float4 (16-byte coalesced loads), per-thread min/max in
+// ordered-int space, warp shuffle reduce, one atomic per warp.
+__global__ void __launch_bounds__(256) range_kernel(const float *__restrict__ x, int64_t n, int32_t *d_range,
+                                                    int32_t *d_flags) {
+    int32_t tmin = INT32_MAX, tmax = INT32_MIN;
+    int nonfinite = 0;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    int64_t head = 0;
+    if (aligned) {
+        const int64_t n4 = n >> 2;
+        const float4 *x4 = reinterpret_cast<const float4 *>(x);
+        for (int64_t i = tid; i < n4; i += stride) {
+            const float4 v = __ldg(x4 + i);
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                nonfinite |= !isfinite(e[q]);
+                const int32_t o = f2ord(e[q]);
+                tmin = min(tmin, o);
+                tmax = max(tmax, o);
+            }
+        }
+        head = n4 << 2;
+    }
+    for (int64_t i = head + tid; i < n; i += stride) {
+        const float v = x[i];
+        nonfinite |= !isfinite(v);
+        const int32_t o = f2ord(v);
+        tmin = min(tmin, o);
+        tmax = max(tmax, o);
+    }
+    range_commit(tmin, tmax, nonfinite, d_range, d_flags, AXB_FLAG_NONFINITE);
+}
+
+__global__ void range_reset_kernel(int32_t *d_range) {
+    d_range[0] = INT32_MAX;
+    d_range[1] = INT32_MIN;
+}
+
+__global__ void coeffs_kernel(const int32_t *d_range, int is_signed, int round_mode, axb_qparams *out) {
+    // an empty/unwritten range (min > max) never reaches here: the host checks flags
+    const float mn = ord2f(d_range[0]);
+    const float mx = ord2f(d_range[1]);
+    *out = coeffs((double)mn, (double)mx, is_signed, round_mode);
+}
+
+__global__ void params_set_kernel(axb_qparams p, axb_qparams *out) { *out = p; }
+
+// ---------------------------------------------------------------- K2: quantize + pad
+// Small-channel mode (cs <= 16): one thread per padded pixel, writes cs bytes.
+template <int CS>
+__global__ void __launch_bounds__(256) quantize_pad_small(const float *__restrict__ x, int64_t n, int64_t h,
+                                                          int64_t w, int c, int pt, int pl, int64_t hp,
+                                                          int64_t wp, const axb_qparams *__restrict__ prm,
+                                                          int is_signed, int round_mode,
+                                                          uint8_t *__restrict__ codes, int32_t *__restrict__ pixsum,
+                                                          int32_t *d_flags) {
+    const double scale = prm->scale;
+    const int zp = prm->zero_point;
+    const int64_t total = n * hp * wp;
+    int nonfinite = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t xw = p % wp;
+        const int64_t t = p / wp;
+        const int64_t yh = t % hp;
+        const int64_t b = t / hp;
+        const int64_t iy = yh - pt, ix = xw - pl;
+        uint8_t outb[CS];
+        int32_t s = 0;
+        if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
+            const float *src = x + ((b * h + iy) * w + ix) * c;
+#pragma unroll
+            for (int ci = 0; ci < CS; ++ci) {
+                if (ci < c) {
+                    const float v = src[ci];
+                    nonfinite |= !isfinite(v);
+                    const int q = quantize_one(v, scale, zp, is_signed, round_mode);
+                    s += q;
+                    outb[ci] = (uint8_t)(q & 0xFF);
+                } else {
+                    outb[ci] = 0;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int ci = 0; ci < CS; ++ci) outb[ci] = ci < c ? (uint8_t)(zp & 0xFF) : (uint8_t)0;
+            s = zp * c;
+        }
+        uint8_t *dst = codes + p * CS;
+        if (CS == 4) {
+            *reinterpret_cast<uint32_t *>(dst) =
+                outb[0] | (outb[1 % CS] << 8) | (outb[2 % CS] << 16) | ((uint32_t)outb[3 % CS] << 24);
+        } else {
+#pragma unroll
+            for (int q = 0; q < CS / 4; ++q)
+                reinterpret_cast<uint32_t *>(dst)[q] = outb[4 * q] | (outb[4 * q + 1] << 8) |
+                                                       (outb[4 * q + 2] << 16) | ((uint32_t)outb[4 * q + 3] << 24);
+        }
+        pixsum[p] = s;
+    }
+    range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
+}
+
+// Wide mode (cs % 16 == 0, cs >= 32): one warp per padded pixel; lane handles
+// 4 channels per step (float4 read, u32 write), warp-reduces the code sum.
+__global__ void __launch_bounds__(256) quantize_pad_wide(const float *__restrict__ x, int64_t n, int64_t h,
+                                                         int64_t w, int c, int64_t cs, int pt, int pl, int64_t hp,
+                                                         int64_t wp, const axb_qparams *__restrict__ prm,
+                                                         int is_signed, int round_mode, uint8_t *__restrict__ codes,
+                                                         int32_t *__restrict__ pixsum, int32_t *d_flags) {
+    const double scale = prm->scale;
+    const int zp = prm->zero_point;
+    const int lane = threadIdx.x & 31;
+    const int64_t total = n * hp * wp;
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool vec = (c % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    int nonfinite = 0;
+    for (int64_t p = warp0; p < total; p += nwarps) {
+        const int64_t xw = p % wp;
+        const int64_t t = p / wp;
+        const int64_t yh = t % hp;
+        const int64_t b = t / hp;
+        const int64_t iy = yh - pt, ix = xw - pl;
+        const bool inside = iy >= 0 && iy < h && ix >= 0 && ix < w;
+        const float *src = x + ((b * h + (inside ? iy : 0)) * w + (inside ? ix : 0)) * c;
+        uint32_t *dst = reinterpret_cast<uint32_t *>(codes + p * cs);
+        int32_t s = 0;
+        for (int64_t g = lane; g < cs / 4; g += 32) {
+            const int64_t c0 = g * 4;
+            uint32_t word = 0;
+            if (inside) {
+                float e[4];
+                if (vec && c0 + 3 < c) {
+                    const float4 v = __ldg(reinterpret_cast<const float4 *>(src + c0));
+                    e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) e[q] = (c0 + q < c) ? src[c0 + q] : 0.0f;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (c0 + q < c) {
+                        nonfinite |= !isfinite(e[q]);
+                        const int qv = quantize_one(e[q], scale, zp, is_signed, round_mode);
+                        s += qv;
+                        word |= (uint32_t)(qv & 0xFF) << (8 * q);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (c0 + q < c) {
+                        s += zp;
+                        word |= (uint32_t)(zp & 0xFF) << (8 * q);
+                    }
+            }
+            dst[g] = word;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) pixsum[p] = s;
+    }
+    range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
+}
+
+// ---------------------------------------------------------------- filters
+// HWCN fp32 -> (kpad, coutp) uint16 = 2 * raw code byte (pre-scaled so the conv
+// kernel builds b<<9 with one PRMT); row k = (ky*kw + kx)*cs + ci.
+__global__ void filters_codes_kernel(const float *__restrict__ f, int64_t kh, int64_t kw, int64_t c, int64_t cout,
+                                     int64_t cs, int64_t kpad, int64_t coutp, const axb_qparams *__restrict__ prm,
+                                     int is_signed, int round_mode, uint16_t *__restrict__ fcodes, int32_t *d_flags) {
+    const double scale = prm->scale;
+    const int zp = prm->zero_point;
+    const int64_t total = kpad * coutp;
+    int nonfinite = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t co = i % coutp;
+        const int64_t k = i / coutp;
+        const int64_t tap = k / cs, ci = k % cs;
+        uint16_t v = 0;
+        if (co < cout && tap < kh * kw && ci < c) {
+            const float fv = f[(tap * c + ci) * cout + co];  // HWCN flat: ((ky*kw+kx)*c+ci)*cout+co
+            nonfinite |= !isfinite(fv);
+            const int q = quantize_one(fv, scale, zp, is_signed, round_mode);
+            v = (uint16_t)((q & 0xFF) << 1);
+        }
+        fcodes[i] = v;
+    }
+    range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
+}
+
+// S_f[co] = sum of code values over the real taps (axconv.py:207), int64 + overflow flag
+__global__ void filters_sum_kernel(const uint16_t *__restrict__ fcodes, int64_t kh, int64_t kw, int64_t c,
+                                   int64_t cout, int64_t cs, int64_t coutp, int is_signed, int64_t *fsum,
+                                   int32_t *d_flags) {
+    const int64_t co = blockIdx.x;
+    int64_t s = 0;
+    const int64_t taps = kh * kw;
+    for (int64_t k = threadIdx.x; k < taps * c; k += blockDim.x) {
+        const int64_t tap = k / c, ci = k % c;
+        const int raw = fcodes[(tap * cs + ci) * coutp + co] >> 1;
+        s += is_signed ? (int)(int8_t)raw : raw;
+    }
+    __shared__ long long red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        fsum[co] = red[0];
+        if (red[0] > INT32_MAX || red[0] < INT32_MIN) atomicOr(d_flags, AXB_FLAG_FSUM_OVF);
+    }
+}
+
+}  // namespace axb
+
+// ======================================================================== C ABI
+using namespace axb;
+
+extern "C" {
+
+int64_t axb_channel_stride(int64_t c) {
+    if (c <= 4) return 4;
+    return (c + 15) / 16 * 16;
+}
+
+int axb_range_reset(int32_t *d_range, void *stream) {
+    range_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_range);
+    return check_launch("range_reset");
+}
+
+int axb_range_minmax(const float *d_x, int64_t n, int32_t *d_range, int32_t *d_flags, void *stream) {
+    if (n <= 0) return set_error(AXB_E_VALUE, "cannot take the range of an empty tensor");
+    int64_t blocks = (n / 4 + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    range_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_x, n, d_range, d_flags);
+    return check_launch("range_minmax");
+}
+
+int axb_range_read(const int32_t *d_range, const int32_t *d_flags, float *mn, float *mx, int32_t *flags,
+                   void *stream) {
+    int32_t r[2] = {0, 0};
+    int32_t fl = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(r, d_range, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return set_error(AXB_E_CUDA, "range readback failed");
+    if (d_flags && cudaMemcpyAsync(&fl, d_flags, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return set_error(AXB_E_CUDA, "flag readback failed");
+    if (cudaStreamSynchronize(s) != cudaSuccess) return set_error(AXB_E_CUDA, "stream sync failed");
+    *mn = ord2f(r[0]);
+    *mx = ord2f(r[1]);
+    if (flags) *flags = fl;
+    return AXB_OK;
+}
+
+int axb_coeffs_host(double mn, double mx, int is_signed, int round_mode, axb_qparams *out) {
+    if (!(mn == mn) || !(mx == mx) || mn - mn != 0.0 || mx - mx != 0.0)
+        return set_error(AXB_E_VALUE, "range must be finite");
+    if (mn > mx) return set_error(AXB_E_VALUE, "range min exceeds max");
+    *out = coeffs(mn, mx, is_signed, round_mode);
+    return AXB_OK;
+}
+
+int axb_coeffs_from_range(const int32_t *d_range, int is_signed, int round_mode, axb_qparams *d_out,
+                          void *stream) {
+    coeffs_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_range, is_signed, round_mode, d_out);
+    return check_launch("coeffs_from_range");
+}
+
+int axb_params_upload(const axb_qparams *host_params, axb_qparams *d_params, void *stream) {
+    params_set_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(*host_params, d_params);
+    return check_launch("params_upload");
+}
+
+int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
+                     int32_t pl, int32_t pr, int64_t cs, const axb_qparams *d_params, int is_signed,
+                     int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags, void *stream) {
+    if (cs != axb_channel_stride(c)) return set_error(AXB_E_VALUE, "channel stride mismatch");
+    const int64_t hp = h + pt + pb, wp = w + pl + pr;
+    const int64_t total = n * hp * wp;
+    if (total == 0) return AXB_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (cs <= 16) {
+        int64_t blocks = (total + 255) / 256;
+        if (blocks > cap) blocks = cap;
+        if (cs == 4)
+            quantize_pad_small<4><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, pt, pl, hp, wp, d_params,
+                                                              is_signed, round_mode, d_codes, d_pixsum, d_flags);
+        else
+            quantize_pad_small<16><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, pt, pl, hp, wp, d_params,
+                                                               is_signed, round_mode, d_codes, d_pixsum, d_flags);
+    } else {
+        int64_t blocks = (total * 32 + 255) / 256;
+        if (blocks > cap) blocks = cap;
+        quantize_pad_wide<<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, cs, pt, pl, hp, wp, d_params, is_signed,
+                                                      round_mode, d_codes, d_pixsum, d_flags);
+    }
+    return check_launch("quantize_pad");
+}
+
+int64_t axb_filter_kpad(int64_t kh, int64_t kw, int64_t cs) { return (kh * kw * cs + 15) / 16 * 16; }
+int64_t axb_filter_coutp(int64_t cout) { return (cout + 15) / 16 * 16; }
+
+int axb_filters_prepare(const float *d_f, int64_t kh, int64_t kw, int64_t c, int64_t cout, int64_t cs,
+                        const axb_qparams *d_params, int is_signed, int round_mode, uint16_t *d_fcodes,
+                        int64_t *d_fsum, int32_t *d_flags, void *stream) {
+    if (cs != axb_channel_stride(c)) return set_error(AXB_E_VALUE, "channel stride mismatch");
+    const int64_t kpad = axb_filter_kpad(kh, kw, cs), coutp = axb_filter_coutp(cout);
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t blocks = (kpad * coutp + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    filters_codes_kernel<<<(int)blocks, 256, 0, s>>>(d_f, kh, kw, c, cout, cs, kpad, coutp, d_params, is_signed,
+                                                      round_mode, d_fcodes, d_flags);
+    if (int e = check_launch("filters_codes")) return e;
+    if (cout > 0) {
+        filters_sum_kernel<<<(int)cout, 256, 0, s>>>(d_fcodes, kh, kw, c, cout, cs, coutp, is_signed, d_fsum,
+                                                      d_flags);
+    }
+    return check_launch("filters_sum");
+}
+
+}  // extern "C"

@@ -1,0 +1,436 @@
+"""GPU executor for transformed AxConv2D graphs (the caller side of the op).
+
+Runs a node list in the reference vocabulary (graph.py:25-37; see
+``resnet.py``) entirely on one CUDA device, stream-ordered, with no host
+synchronisation until the final flag check:
+
+* ``Min``/``Max`` range nodes (graph.py:270-275) are fused into whoever
+  produces the tensor: the conv epilogue, the pool / add kernels, or a
+  standalone range kernel (K1) for the graph input.  Ranges stay on device;
+  coefficients are computed on device (``axb_coeffs_from_range``).
+* ``AxConv2D`` (graph.py:248-269) = K2 quantize/zp-pad + K3 LUT implicit GEMM
+  whose epilogue also applies the bias and, when the graph allows it, the
+  residual ``Add`` (graph.py:282-286) and ``ReLU`` (graph.py:276-277).
+  IEEE fp32 addition is commutative, so ``Add(a, b)`` may be fused into the
+  producer of either operand -- the later one in node order is chosen so the
+  other operand already exists.
+* ``MaxPool``/``AvgPool`` (graph.py:182-199), stand-alone ``ReLU``/``Add``:
+  small float-glue kernels with numpy-identical arithmetic order.
+* ``Flatten``/``Dense``/``Softmax`` run as torch ops (float glue, not
+  bit-reproducible against numpy BLAS -- the benchmark graphs use a 1x1
+  AxConv2D classifier instead).
+
+Non-finite values reaching a range node raise ``ValueError`` like the
+reference (checked once, at the end of ``run``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .axconv import device_lut
+from .types import ConvGeometry, _mode_value, is_signed, output_shape, resolve_padding
+
+_I32_MAX = 2**31 - 1
+_I32_MIN = -(2**31)
+
+
+def _geometry(attrs) -> ConvGeometry:
+    pad = attrs.get("padding", "valid")
+    if isinstance(pad, list):
+        pad = tuple(pad)
+    return ConvGeometry(tuple(attrs.get("strides", (1, 1))), tuple(attrs.get("dilations", (1, 1))), pad)
+
+
+def _pool_geometry(attrs):
+    ph, pw = tuple(attrs.get("pool", (2, 2)))
+    pad = attrs.get("padding", "valid")
+    if isinstance(pad, list):
+        pad = tuple(pad)
+    return ph, pw, ConvGeometry(tuple(attrs.get("strides", (ph, pw))), (1, 1), pad)
+
+
+@dataclass
+class _ConvPlan:
+    node: dict
+    x: str                      # data input tensor id
+    out: str                    # tensor id the fused epilogue writes
+    relu: bool = False
+    residual: str | None = None
+    geometry: ConvGeometry = None
+    in_shape: tuple = ()
+    out_shape: tuple = ()
+    pads: tuple = ()
+    kh: int = 0
+    kw: int = 0
+    cin: int = 0
+    cout: int = 0
+    cs: int = 0
+    kpad: int = 0
+    coutp: int = 0
+    lut: object = None
+    fcodes: torch.Tensor = None
+    fsum: torch.Tensor = None
+    bias: torch.Tensor | None = None
+    params: torch.Tensor = None  # [in, f] axb_qparams as 2 x 16 bytes
+
+
+@dataclass
+class _Step:
+    kind: str
+    node: dict
+    plan: _ConvPlan | None = None
+    extra: dict = field(default_factory=dict)
+
+
+class GpuGraph:
+    """Prepared graph: filters quantized once (hoisted, cf. axconv.py:287), fusion planned."""
+
+    def __init__(self, nodes, device=None, accumulator="exact64", round_mode="half-away-from-zero",
+                 in_shape=None, sm_limit: int = 0):
+        if not torch.cuda.is_available():
+            raise _lib.AxbError("GpuGraph needs a CUDA device (no CPU fallback)")
+        self.nodes = list(nodes)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.acc = _lib.ACC[_mode_value(accumulator)]
+        self.round = _lib.ROUND[_mode_value(round_mode)]
+        self.sm_limit = int(sm_limit)
+        self.lib = _lib.load()
+        self._plan()
+
+    # ------------------------------------------------------------------ planning
+    def _plan(self):
+        nodes = self.nodes
+        ids = [n["id"] for n in nodes]
+        if len(set(ids)) != len(ids):
+            raise ValueError("duplicate node id")
+        self.by_id = {n["id"]: n for n in nodes}
+        order = {nid: i for i, nid in enumerate(ids)}
+        consumers: dict[str, list[str]] = {nid: [] for nid in ids}
+        for n in nodes:
+            for i in n.get("inputs", []):
+                if i not in consumers:
+                    raise ValueError(f"node {n['id']!r} references {i!r} which does not precede it")
+                consumers[i].append(n["id"])
+        self.consumers = consumers
+        alias: dict[str, str] = {}  # node id -> tensor id holding its value
+
+        def t(nid):
+            while nid in alias:
+                nid = alias[nid]
+            return nid
+
+        fused_away: set[str] = set()
+        conv_plans: dict[str, _ConvPlan] = {}
+        for n in nodes:
+            if n["kind"] == "AxConv2D":
+                if len(n["inputs"]) != 3:
+                    raise ValueError(f"AxConv2D node {n['id']!r} needs data, min, and max inputs")
+                conv_plans[n["id"]] = _ConvPlan(node=n, x=n["inputs"][0], out=n["id"])
+        # Add fusion: pick the later-produced conv operand with a single consumer
+        for n in nodes:
+            if n["kind"] != "Add":
+                continue
+            a, b = n["inputs"]
+            cands = [v for v in (a, b) if v in conv_plans and consumers[v] == [n["id"]]
+                     and not conv_plans[v].relu and conv_plans[v].residual is None]
+            if not cands:
+                continue
+            host = max(cands, key=lambda v: order[v])
+            other = b if host == a else a
+            if order[other] > order[host] and other not in ("",):
+                continue
+            p = conv_plans[host]
+            p.residual = other
+            alias[n["id"]] = host
+            fused_away.add(n["id"])
+            cons = consumers[n["id"]]
+            if len(cons) == 1 and self.by_id[cons[0]]["kind"] == "ReLU":
+                p.relu = True
+                alias[cons[0]] = host
+                fused_away.add(cons[0])
+        # ReLU fusion directly after a conv
+        for n in nodes:
+            if n["kind"] == "ReLU" and n["id"] not in fused_away:
+                src = n["inputs"][0]
+                if src in conv_plans and consumers[src] == [n["id"]] and not conv_plans[src].relu:
+                    conv_plans[src].relu = True
+                    alias[n["id"]] = src
+                    fused_away.add(n["id"])
+        self.alias = alias
+        self.t = t
+        # tensors that need a device range (inputs of Min/Max nodes)
+        need_range = set()
+        for n in nodes:
+            if n["kind"] in ("Min", "Max"):
+                need_range.add(t(n["inputs"][0]))
+        self.need_range = need_range
+        tensor_ids = sorted({t(nid) for nid in ids}, key=lambda v: order[v])
+        self.slot = {tid: i for i, tid in enumerate(tensor_ids)}
+        self.ranges_template = torch.tensor([[_I32_MAX, _I32_MIN]] * len(tensor_ids), dtype=torch.int32,
+                                            device=self.device)
+        self.ranges = self.ranges_template.clone()
+        self.flags = torch.zeros(len(tensor_ids) + 1, dtype=torch.int32, device=self.device)
+        # steps
+        self.steps: list[_Step] = []
+        for n in nodes:
+            kind = n["kind"]
+            if n["id"] in fused_away or kind in ("Min", "Max"):
+                continue
+            if kind == "AxConv2D":
+                self.steps.append(_Step("conv", n, conv_plans[n["id"]]))
+            elif kind in ("Input", "ReLU", "Add", "MaxPool", "AvgPool", "Flatten", "Dense", "Softmax"):
+                self.steps.append(_Step(kind, n))
+            else:
+                raise ValueError(f"unsupported node kind {kind!r}")
+        self.conv_plans = conv_plans
+        self._prepared_for = None
+
+    def _prepare_shapes(self, in_shape):
+        """Shape inference + one-time filter preparation for this input shape."""
+        if self._prepared_for == tuple(in_shape):
+            return
+        shapes = {}
+        for st in self.steps:
+            n = st.node
+            a = n.get("attrs", {})
+            if st.kind == "Input":
+                want = a.get("shape")
+                if want is not None and tuple(want) != tuple(in_shape[1:]):
+                    raise ValueError(f"input shape {tuple(in_shape[1:])} does not match graph {tuple(want)}")
+                shapes[n["id"]] = tuple(in_shape)
+            elif st.kind == "conv":
+                p = st.plan
+                xs = shapes[self.t(p.x)]
+                f = a["filters"]
+                p.geometry = _geometry(a)
+                p.in_shape = xs
+                p.out_shape = output_shape(xs, f.shape, p.geometry)
+                p.kh, p.kw, p.cin, p.cout = (int(v) for v in f.shape)
+                p.pads = resolve_padding(p.geometry, xs[1], xs[2], p.kh, p.kw)
+                shapes[n["id"]] = p.out_shape
+                if p.fcodes is None:
+                    self._prepare_filters(p, a)
+            elif st.kind in ("ReLU", "Add"):
+                shapes[n["id"]] = shapes[self.t(n["inputs"][0])]
+            elif st.kind in ("MaxPool", "AvgPool"):
+                xs = shapes[self.t(n["inputs"][0])]
+                ph, pw, geo = _pool_geometry(a)
+                o = output_shape(xs, (ph, pw, xs[3], 1), geo)
+                shapes[n["id"]] = (xs[0], o[1], o[2], xs[3])
+                st.extra = dict(ph=ph, pw=pw, geo=geo, pads=resolve_padding(geo, xs[1], xs[2], ph, pw))
+            elif st.kind == "Flatten":
+                xs = shapes[self.t(n["inputs"][0])]
+                shapes[n["id"]] = (xs[0], int(np.prod(xs[1:])))
+            elif st.kind == "Dense":
+                xs = shapes[self.t(n["inputs"][0])]
+                shapes[n["id"]] = (xs[0], a["weights"].shape[1])
+            elif st.kind == "Softmax":
+                shapes[n["id"]] = shapes[self.t(n["inputs"][0])]
+        self.shapes = shapes
+        self._prepared_for = tuple(in_shape)
+
+    def _prepare_filters(self, p: _ConvPlan, a):
+        lib = self.lib
+        p.lut = device_lut(a["lut"], self.device.index)
+        sgn = int(p.lut.signed)
+        p.cs = int(lib.axb_channel_stride(p.cin))
+        p.kpad = int(lib.axb_filter_kpad(p.kh, p.kw, p.cs))
+        p.coutp = int(lib.axb_filter_coutp(p.cout))
+        f = torch.from_numpy(np.ascontiguousarray(a["filters"], dtype=np.float32)).to(self.device)
+        p.params = torch.zeros(2, 16, dtype=torch.uint8, device=self.device)
+        hp = _lib.QParams()
+        _lib.check(lib.axb_coeffs_host(float(a["f_min"]), float(a["f_max"]), sgn, self.round, hp))
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(lib.axb_params_upload(hp, p.params[1].data_ptr(), stream))
+        p.fcodes = torch.empty(p.kpad * p.coutp, dtype=torch.int16, device=self.device)
+        p.fsum = torch.empty(max(p.cout, 1), dtype=torch.int64, device=self.device)
+        fl = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.check(lib.axb_filters_prepare(f.data_ptr(), p.kh, p.kw, p.cin, p.cout, p.cs, p.params[1].data_ptr(),
+                                           sgn, self.round, p.fcodes.data_ptr(), p.fsum.data_ptr(),
+                                           fl.data_ptr(), stream))
+        flags = int(fl.item())
+        if flags & _lib.FLAG_NONFINITE:
+            raise ValueError("cannot quantize non-finite values")
+        if flags & _lib.FLAG_FSUM_OVF:
+            raise OverflowError("filter size too large for 32-bit code sums")
+        b = a.get("bias")
+        p.bias = None if b is None else torch.from_numpy(np.ascontiguousarray(b, np.float32)).to(self.device)
+
+    # ------------------------------------------------------------------ execution
+    def run(self, batch: torch.Tensor, check: bool = True, trace: dict | None = None,
+            profile: list | None = None) -> torch.Tensor:
+        """Evaluate on a (n,h,w,c) fp32 CUDA batch; returns the last node's value.
+
+        ``profile`` (a list) receives (node_id, start_event, end_event, macs)
+        around every LUT-conv kernel launch, for live per-kernel timing.
+        """
+        if batch.dim() != 4:
+            raise ValueError("batch must be NHWC")
+        batch = batch.to(self.device, torch.float32).contiguous()
+        self._prepare_shapes(tuple(batch.shape))
+        lib = self.lib
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.ranges.copy_(self.ranges_template)
+        self.flags.zero_()
+        self.launches = 0  # libaxb kernels launched by this run
+        self._profile = profile
+        vals: dict[str, torch.Tensor] = {}
+        remaining = {tid: 0 for tid in self.slot}
+        for n in self.nodes:
+            for i in n.get("inputs", []):
+                remaining[self.t(i)] += 1
+        last = None
+
+        def rng_ptr(tid):
+            return self.ranges[self.slot[tid]].data_ptr() if tid in self.need_range else None
+
+        def flag_ptr(tid):
+            return self.flags[self.slot[tid]].data_ptr()
+
+        def release(n):
+            if trace is not None:
+                return
+            for i in n.get("inputs", []):
+                tid = self.t(i)
+                remaining[tid] -= 1
+                if remaining[tid] == 0 and tid in vals and tid != last:
+                    del vals[tid]
+
+        for st in self.steps:
+            n = st.node
+            nid = n["id"]
+            if st.kind == "Input":
+                vals[nid] = batch
+                if nid in self.need_range:
+                    if batch.numel() == 0:
+                        raise ValueError("cannot take the range of an empty tensor")
+                    _lib.check(lib.axb_range_minmax(batch.data_ptr(), batch.numel(), rng_ptr(nid),
+                                                    flag_ptr(nid), stream))
+                    self.launches += 1
+            elif st.kind == "conv":
+                vals[nid] = self._run_conv(st.plan, vals, rng_ptr(nid), flag_ptr(nid), stream)
+            elif st.kind in ("ReLU", "Add"):
+                a = vals[self.t(n["inputs"][0])]
+                b = vals[self.t(n["inputs"][1])] if st.kind == "Add" else None
+                if b is not None and a.shape != b.shape:
+                    raise ValueError(f"Add node {nid!r} input shapes differ")
+                out = torch.empty_like(a)
+                _lib.check(lib.axb_add_relu(a.data_ptr(), b.data_ptr() if b is not None else None, a.numel(),
+                                            int(st.kind == "ReLU"), out.data_ptr(), rng_ptr(nid), flag_ptr(nid),
+                                            stream))
+                self.launches += 1
+                vals[nid] = out
+            elif st.kind in ("MaxPool", "AvgPool"):
+                x = vals[self.t(n["inputs"][0])]
+                e = st.extra
+                os_ = self.shapes[nid]
+                out = torch.empty(os_, dtype=torch.float32, device=self.device)
+                fn = lib.axb_maxpool if st.kind == "MaxPool" else lib.axb_avgpool
+                _lib.check(fn(x.data_ptr(), *x.shape, e["ph"], e["pw"], e["geo"].strides[0], e["geo"].strides[1],
+                              e["pads"][0], e["pads"][2], os_[1], os_[2], out.data_ptr(), rng_ptr(nid),
+                              flag_ptr(nid), stream))
+                self.launches += 1
+                vals[nid] = out
+            elif st.kind == "Flatten":
+                x = vals[self.t(n["inputs"][0])]
+                vals[nid] = x.reshape(x.shape[0], -1)
+            elif st.kind == "Dense":
+                x = vals[self.t(n["inputs"][0])]
+                if x.dim() != 2:
+                    raise ValueError(f"Dense node {nid!r} expects a flattened input")
+                w = torch.from_numpy(np.asarray(n["attrs"]["weights"], np.float32)).to(self.device)
+                y = x @ w
+                if n["attrs"].get("bias") is not None:
+                    y = y + torch.from_numpy(np.asarray(n["attrs"]["bias"], np.float32)).to(self.device)
+                vals[nid] = y
+                if nid in self.need_range:
+                    _lib.check(lib.axb_range_minmax(y.data_ptr(), y.numel(), rng_ptr(nid), flag_ptr(nid), stream))
+            elif st.kind == "Softmax":
+                x = vals[self.t(n["inputs"][0])]
+                vals[nid] = torch.softmax(x, dim=-1)
+            last = self.t(nid)
+            release(n)
+        out = vals[last]
+        if check:
+            self.check_flags()
+        if trace is not None:
+            for n in self.nodes:
+                if n["kind"] not in ("Min", "Max"):
+                    trace[n["id"]] = vals[self.t(n["id"])]
+        if out.dim() == 2:
+            out = out.reshape(out.shape[0], 1, 1, out.shape[1])
+        return out
+
+    def check_flags(self):
+        fl = self.flags.cpu().numpy()
+        for n in self.nodes:
+            if n["kind"] in ("Min", "Max"):
+                tid = self.t(n["inputs"][0])
+                if fl[self.slot[tid]] & (_lib.FLAG_NONFINITE | _lib.FLAG_OUT_NONFINITE):
+                    raise ValueError(f"non-finite values reaching {n['id']!r}")
+        for n in self.nodes:
+            if n["kind"] == "AxConv2D":
+                if fl[self.slot[self.t(n["id"])]] & _lib.FLAG_PSUM_OVF:
+                    raise OverflowError("patch length too large for 32-bit code sums")
+
+    def _run_conv(self, p: _ConvPlan, vals, out_range, out_flag, stream):
+        lib = self.lib
+        x = vals[self.t(p.x)]
+        n, h, w, c = p.in_shape
+        _, oh, ow, cout = p.out_shape
+        out = torch.empty(p.out_shape, dtype=torch.float32, device=self.device)
+        if n == 0:
+            return out
+        sgn = int(p.lut.signed)
+        pt, pb, pl, pr = p.pads
+        hp, wp = h + pt + pb, w + pl + pr
+        codes = torch.empty(n * hp * wp * p.cs, dtype=torch.uint8, device=self.device)
+        pixsum = torch.empty(n * hp * wp, dtype=torch.int32, device=self.device)
+        xr = self.ranges[self.slot[self.t(p.x)]].data_ptr()
+        _lib.check(lib.axb_coeffs_from_range(xr, sgn, self.round, p.params[0].data_ptr(), stream))
+        qflag = self.flags[len(self.slot)].data_ptr()
+        _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, p.cs, p.params[0].data_ptr(),
+                                        sgn, self.round, codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
+        d = _lib.ConvDesc()
+        d.codes, d.pixsum = codes.data_ptr(), pixsum.data_ptr()
+        d.n, d.hp, d.wp, d.cs, d.c = n, hp, wp, p.cs, c
+        d.kh, d.kw = p.kh, p.kw
+        d.sh, d.sw = p.geometry.strides
+        d.dh, d.dw = p.geometry.dilations
+        d.oh, d.ow = oh, ow
+        d.fcodes, d.fsum = p.fcodes.data_ptr(), p.fsum.data_ptr()
+        d.cout, d.coutp, d.kpad = cout, p.coutp, p.kpad
+        d.in_params, d.f_params = p.params[0].data_ptr(), p.params[1].data_ptr()
+        d.accumulator = self.acc
+        d.relu = int(p.relu)
+        d.bias = p.bias.data_ptr() if p.bias is not None else None
+        if p.residual is not None:
+            r = vals[self.t(p.residual)]
+            if tuple(r.shape) != tuple(p.out_shape):
+                raise ValueError(f"Add input shapes differ at {p.node['id']!r}")
+            d.residual = r.data_ptr()
+        d.out = out.data_ptr()
+        d.out_range = out_range
+        d.flags = out_flag
+        d.sm_limit = self.sm_limit
+        prof = self._profile
+        if prof is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        _lib.check(lib.axb_conv2d_lut(d, p.lut.handle, stream))
+        if prof is not None:
+            e1.record()
+            prof.append((p.node["id"], e0, e1, n * oh * ow * p.kh * p.kw * c * cout))
+        self.launches += 3  # coeffs, quantize, conv
+        return out
+
+
+def run(nodes, batch, **kw) -> torch.Tensor:
+    """One-shot helper: GpuGraph(nodes).run(batch)."""
+    return GpuGraph(nodes, **{k: v for k, v in kw.items() if k in ("device", "accumulator", "round_mode")}).run(
+        batch if isinstance(batch, torch.Tensor) else torch.from_numpy(np.asarray(batch, np.float32)))
