@@ -128,9 +128,23 @@ typedef struct axb_conv_desc {
     int32_t *flags;         /* device int32 flag word                               */
     int32_t force_generic;  /* 1: use the int64 generic kernel (testing)            */
     int32_t sm_limit;       /* 0 = all SMs; else cap persistent grid                 */
+    int32_t variant;        /* fast-kernel tile variant, 0 = heuristic (tuning)      */
 } axb_conv_desc;
 
 int axb_conv2d_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);
+int axb_conv_variant_count(void);
+const char *axb_conv_variant_name(int variant);
+
+/* ---- small-channel layers: explicit im2col of the codes (axconv.py:160-196) ----
+ * When c is not a multiple of 16 and the kernel has >1 tap, zero-channel
+ * padding would waste most lookups; instead the zp-padded codes are gathered
+ * into dense rows of kp = roundup16(kh*kw*c) bytes (row sum = patch sum S_p)
+ * and the conv runs as a 1x1 over (n, oh, ow, kp) with c = kh*kw*c.
+ * axb_conv_im2col_kp returns kp when that path applies, else 0. */
+int64_t axb_conv_im2col_kp(int64_t c, int64_t kh, int64_t kw);
+int axb_im2col_pack(const uint8_t *d_codes, int64_t n, int64_t hp, int64_t wp, int64_t cs, int64_t c, int32_t kh,
+                    int32_t kw, int32_t sh, int32_t sw, int32_t dh, int32_t dw, int64_t oh, int64_t ow, int64_t kp,
+                    int is_signed, uint8_t *d_rows, int32_t *d_rowsum, void *stream);
 /* which kernel variant the last axb_conv2d_lut call on this thread launched */
 const char *axb_last_kernel(void);
 

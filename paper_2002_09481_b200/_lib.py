@@ -53,7 +53,7 @@ class ConvDesc(ctypes.Structure):
         ("accumulator", c_i32), ("relu", c_i32),
         ("bias", c_vp), ("residual", c_vp), ("out", c_vp), ("acc_out", c_vp),
         ("out_range", c_vp), ("flags", c_vp),
-        ("force_generic", c_i32), ("sm_limit", c_i32),
+        ("force_generic", c_i32), ("sm_limit", c_i32), ("variant", c_i32),
     ]
 
 
@@ -81,6 +81,11 @@ SIGNATURES = {
     "axb_filters_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_int, c_int, c_vp,
                                     c_vp, c_vp, c_vp]),
     "axb_conv2d_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
+    "axb_conv_variant_count": (c_int, []),
+    "axb_conv_variant_name": (ctypes.c_char_p, [c_int]),
+    "axb_conv_im2col_kp": (c_i64, [c_i64, c_i64, c_i64]),
+    "axb_im2col_pack": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_vp]),
     "axb_axconv2d": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i32, c_i32,
                              c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_dbl, c_dbl, c_dbl, c_dbl, c_i32,
                              c_i32, c_vp, c_vp, c_vp, c_vp]),

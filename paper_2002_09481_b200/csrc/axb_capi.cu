@@ -249,10 +249,13 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
     const int64_t oh = (hp - ekh) / sh + 1, ow = (wp - ekw) / sw + 1;
     if (n == 0 || cout == 0) return AXB_OK;
     const int64_t cs = axb_channel_stride(c);
-    const int64_t kpad = axb_filter_kpad(kh, kw, cs), coutp = axb_filter_coutp(cout);
+    const int64_t kp = axb_conv_im2col_kp(c, kh, kw);  // small-channel layers: explicit im2col rows
+    // filter geometry as the conv kernel sees it: (1,1,K) over kp-byte rows, or (kh,kw,c) over cs
+    const int64_t fkh = kp ? 1 : kh, fkw = kp ? 1 : kw, fc = kp ? kh * kw * c : c, fcs = kp ? kp : cs;
+    const int64_t kpad = axb_filter_kpad(fkh, fkw, fcs), coutp = axb_filter_coutp(cout);
 
-    uint8_t *codes = nullptr;
-    int32_t *pixsum = nullptr, *flags = nullptr;
+    uint8_t *codes = nullptr, *rows = nullptr;
+    int32_t *pixsum = nullptr, *flags = nullptr, *rowsum = nullptr;
     axb_qparams *dp = nullptr;
     uint16_t *fcodes = nullptr;
     int64_t *fsum = nullptr;
@@ -264,7 +267,9 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
         cudaMallocAsync(&pixsum, n * hp * wp * 4, s) != cudaSuccess ||
         cudaMallocAsync(&flags, 8, s) != cudaSuccess || cudaMallocAsync(&dp, 2 * sizeof(axb_qparams), s) != cudaSuccess ||
         cudaMallocAsync(&fcodes, kpad * coutp * 2, s) != cudaSuccess ||
-        cudaMallocAsync(&fsum, (cout > 0 ? cout : 1) * 8, s) != cudaSuccess) {
+        cudaMallocAsync(&fsum, (cout > 0 ? cout : 1) * 8, s) != cudaSuccess ||
+        (kp && (cudaMallocAsync(&rows, n * oh * ow * kp, s) != cudaSuccess ||
+                cudaMallocAsync(&rowsum, n * oh * ow * 4, s) != cudaSuccess))) {
         fail(AXB_E_CUDA, "device allocation failed");
     }
     if (rc == AXB_OK) {
@@ -272,18 +277,28 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
         if (int e = axb_params_upload(&p1, dp, s)) rc = e;
         if (!rc) rc = axb_params_upload(&p2, dp + 1, s);
         if (!rc)
-            rc = axb_filters_prepare(d_f, kh, kw, c, cout, cs, dp + 1, sgn, round_mode, fcodes, fsum, flags, s);
+            rc = axb_filters_prepare(d_f, fkh, fkw, fc, cout, fcs, dp + 1, sgn, round_mode, fcodes, fsum, flags, s);
     }
     if (!rc)
         rc = axb_quantize_pad(d_x, n, h, w, c, pt, pb, pl, pr, cs, dp, sgn, round_mode, codes, pixsum, flags + 1,
                               s);
+    if (!rc && kp)
+        rc = axb_im2col_pack(codes, n, hp, wp, cs, c, (int32_t)kh, (int32_t)kw, sh, sw, dh, dw, oh, ow, kp, sgn, rows,
+                             rowsum, s);
     if (!rc) {
         axb_conv_desc d;
         memset(&d, 0, sizeof d);
-        d.codes = codes;
-        d.pixsum = pixsum;
-        d.n = n; d.hp = hp; d.wp = wp; d.cs = cs; d.c = c;
-        d.kh = (int32_t)kh; d.kw = (int32_t)kw; d.sh = sh; d.sw = sw; d.dh = dh; d.dw = dw;
+        if (kp) {
+            d.codes = rows;
+            d.pixsum = rowsum;
+            d.n = n; d.hp = oh; d.wp = ow; d.cs = kp; d.c = kh * kw * c;
+            d.kh = d.kw = d.sh = d.sw = d.dh = d.dw = 1;
+        } else {
+            d.codes = codes;
+            d.pixsum = pixsum;
+            d.n = n; d.hp = hp; d.wp = wp; d.cs = cs; d.c = c;
+            d.kh = (int32_t)kh; d.kw = (int32_t)kw; d.sh = sh; d.sw = sw; d.dh = dh; d.dw = dw;
+        }
         d.oh = oh; d.ow = ow;
         d.fcodes = fcodes; d.fsum = fsum; d.cout = cout; d.coutp = coutp; d.kpad = kpad;
         d.in_params = dp; d.f_params = dp + 1;
@@ -304,6 +319,8 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
     }
     cudaFreeAsync(codes, s);
     cudaFreeAsync(pixsum, s);
+    if (rows) cudaFreeAsync(rows, s);
+    if (rowsum) cudaFreeAsync(rowsum, s);
     cudaFreeAsync(flags, s);
     cudaFreeAsync(dp, s);
     cudaFreeAsync(fcodes, s);

@@ -148,16 +148,23 @@ __device__ __forceinline__ void track(float y, int32_t &tmin, int32_t &tmax, int
 }
 
 // ---------------------------------------------------------------- fast kernel
-template <int TM, int WM, int WN, bool SGN, int SEG>
-__global__ void __launch_bounds__(kThreads, 1) lutconv_fast(const ConvK p) {
+// Persistent CTA (one per SM, the LUT takes 128 KiB of its shared memory).
+// The CTA walks its tiles (tile = blockIdx.x + j*gridDim.x) and their 16-tap
+// chunks as ONE continuous stream of iterations, so the cp.async ring keeps
+// prefetching the next tile's first chunks while the current tile finishes
+// and runs its epilogue (no per-tile pipeline fill / drain).
+template <int TM, int TN, int WM, int WN, bool SGN>
+__global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
+    constexpr int NT = WM * WN * 32;
     constexpr int BM = WM * 32 * TM;
-    constexpr int BN = WN * 16;
+    constexpr int BN = WN * TN;
     constexpr int ACT_STAGE = BM * 16;
     constexpr int W_STAGE = 16 * BN * 2;
-    constexpr int SEGS = 16 / SEG;                  // segments per act row per chunk
-    constexpr int NQ = BM * SEGS / kThreads;        // act cp.async per thread per chunk
-    static_assert(NQ >= 1 && (BM * SEGS) % kThreads == 0, "tile/thread mismatch");
-    static_assert(WM * WN * 32 == kThreads, "8 warps");
+    constexpr int NQ = BM / NT;  // activation rows per thread per chunk (one 16-byte cp.async each)
+    constexpr int WG = TN / 8;   // 16-byte weight groups per tap per warp
+    static_assert(BM % NT == 0 && NQ >= 1, "tile/thread mismatch");
+    static_assert(2 * BN <= NT, "one weight piece per thread");
+    static_assert(TN % 8 == 0, "TN multiple of 8");
 
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *act_s = smem + kLutBytes;
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1) lutconv_fast(const ConvK p) {
     const int wn = warp / WM;
 
     if (tid == 0) mbar_init(bar, 1);
-    for (int t = tid; t < p.taps; t += kThreads) {
+    for (int t = tid; t < p.taps; t += NT) {
         const int ky = t / p.kw, kx = t % p.kw;
         const int pix = ky * p.dh * p.wp + kx * p.dw;
         tappix_s[t] = pix;
@@ -181,29 +188,32 @@ __global__ void __launch_bounds__(kThreads, 1) lutconv_fast(const ConvK p) {
     }
     __syncthreads();
     if (tid == 0) {
-        // stage the whole table with 4 TMA bulk copies (32 KiB each)
+        // the whole 128 KiB table in 4 TMA bulk copies (32 KiB each), completion on one mbarrier
         mbar_expect_tx(bar, kLutBytes);
 #pragma unroll
         for (int q = 0; q < 4; ++q) bulk_g2s(smem + q * 32768, p.lut + q * 16384, 32768, bar);
     }
-    bool lut_ready = false;
 
     const EpiConst e = epi_const(p);
     int32_t tmin = INT32_MAX, tmax = INT32_MIN;
     int nonfinite = 0, psum_ovf = 0;
     const uint32_t lut_base = smem_u32(smem);
 
-    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-        const int64_t m0 = (tile / p.ntn) * BM;
-        const int n0 = (int)(tile % p.ntn) * BN;
+    const int64_t my_tiles = (p.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t total = my_tiles * p.nchunks;
 
-        // per-thread gather rows for this tile (pixel base offsets into the code tensor)
-        int32_t rowbase[NQ];
+    // ---- producer state (runs kStages-1 iterations ahead of the consumer)
+    int64_t ld_it = 0;
+    int ld_kc = 0;
+    int64_t ld_tile = blockIdx.x;
+    int ld_n0 = 0;
+    int32_t rowbase[NQ];
+    auto set_load_tile = [&](int64_t tile) {
+        const int64_t m0 = (tile / p.ntn) * BM;
+        ld_n0 = (int)(tile % p.ntn) * BN;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            const int item = tid + q * kThreads;
-            const int row = item / SEGS;
-            const int64_t m = m0 + row;
+            const int64_t m = m0 + tid + q * NT;
             if (m < p.M) {
                 const int64_t ox = m % p.ow;
                 const int64_t t = m / p.ow;
@@ -214,156 +224,155 @@ __global__ void __launch_bounds__(kThreads, 1) lutconv_fast(const ConvK p) {
                 rowbase[q] = -1;
             }
         }
-
-        auto load_stage = [&](int stage, int kc) {
+    };
+    set_load_tile(ld_tile);
+    auto load_next = [&]() {
+        if (ld_it < total) {
+            const int stage = (int)(ld_it % kStages);
             uint8_t *as = act_s + stage * ACT_STAGE;
-            if (SEG == 16) {
-                const int k0 = kc * 16;
-                const int t = k0 / p.cs;
-                const int ci = k0 - t * p.cs;
-                const bool tv = t < p.taps;
-                const int off = tv ? tapoff_s[t] + ci : 0;
+            const int k0 = ld_kc * 16;
+            const int t = k0 / p.cs;
+            const int ci = k0 - t * p.cs;
+            const bool tv = t < p.taps;
+            const int off = tv ? tapoff_s[t] + ci : 0;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int row = tid + q * kThreads;
-                    const bool v = tv && rowbase[q] >= 0;
-                    const uint8_t *src = p.codes + (v ? (int64_t)rowbase[q] + off : 0);
-                    cp_async16(as + row * 16, src, v ? 16 : 0);
-                }
-            } else {  // SEG == 4: cs == 4, one tap per 4-byte segment
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int item = tid + q * kThreads;
-                    const int row = item >> 2, seg = item & 3;
-                    const int t = kc * 4 + seg;
-                    const bool v = t < p.taps && rowbase[q] >= 0;
-                    const uint8_t *src = p.codes + (v ? (int64_t)rowbase[q] + tapoff_s[t] : 0);
-                    cp_async4(as + row * 16 + seg * 4, src, v ? 4 : 0);
-                }
+            for (int q = 0; q < NQ; ++q) {
+                const bool v = tv && rowbase[q] >= 0;
+                const uint8_t *src = p.codes + (v ? (int64_t)rowbase[q] + off : 0);
+                cp_async16(as + (tid + q * NT) * 16, src, v ? 16 : 0);
             }
             if (tid < 2 * BN) {
                 uint8_t *ws = w_s + stage * W_STAGE;
                 const int r = tid / (BN / 8);
                 const int col = (tid % (BN / 8)) * 8;
-                const int gcol = n0 + col;
+                const int gcol = ld_n0 + col;
                 const bool v = gcol < p.coutp;
-                const uint16_t *src = p.fcodes + (v ? (int64_t)(kc * 16 + r) * p.coutp + gcol : 0);
+                const uint16_t *src = p.fcodes + (v ? (int64_t)(k0 + r) * p.coutp + gcol : 0);
                 cp_async16(ws + (r * BN + col) * 2, src, v ? 16 : 0);
             }
-        };
-
-        int32_t acc[TM][16];
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[i][j] = 0;
-
-#pragma unroll
-        for (int s = 0; s < kStages - 1; ++s) {
-            if (s < p.nchunks) load_stage(s, s);
-            cp_async_commit();
-        }
-        if (!lut_ready) {
-            mbar_wait(bar, 0);
-            lut_ready = true;
-        }
-
-        for (int kc = 0; kc < p.nchunks; ++kc) {
-            cp_async_wait<kStages - 2>();
-            __syncthreads();
-            {
-                const int nk = kc + kStages - 1;
-                if (nk < p.nchunks) load_stage(nk % kStages, nk);
-                cp_async_commit();
+            ++ld_it;
+            if (++ld_kc == p.nchunks) {
+                ld_kc = 0;
+                ld_tile += gridDim.x;
+                if (ld_it < total) set_load_tile(ld_tile);
             }
-            const int stage = kc % kStages;
-            const uint8_t *as = act_s + stage * ACT_STAGE;
-            const uint8_t *ws = w_s + stage * W_STAGE + wn * 32;
-            uint4 av[TM];
+        }
+        cp_async_commit();
+    };
+
+    int32_t acc[TM][TN];
 #pragma unroll
-            for (int i = 0; i < TM; ++i)
-                av[i] = *reinterpret_cast<const uint4 *>(as + (wm * 32 * TM + i * 32 + lane) * 16);
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0;
+
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) load_next();
+    mbar_wait(bar, 0);
+
+    int c_kc = 0;
+    int64_t c_tile = blockIdx.x;
+    for (int64_t it = 0; it < total; ++it) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        load_next();
+        const int stage = (int)(it % kStages);
+        const uint8_t *as = act_s + stage * ACT_STAGE + (wm * 32 * TM + lane) * 16;
+        const uint8_t *ws = w_s + stage * W_STAGE + wn * TN * 2;
+        uint4 av[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const uint4 *>(as + i * 32 * 16);
 
 #pragma unroll 1
-            for (int kp = 0; kp < 8; ++kp) {  // two taps per step: kk = 2kp, 2kp+1
-                const int q = kp >> 1;
-                const uint32_t s0 = 0x4440u + ((kp & 1) << 1);
-                uint32_t a0[TM], a1[TM];
+        for (int q = 0; q < 4; ++q) {  // 4 taps per step, consumed as 2 pairs
+            uint32_t aw[TM];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) aw[i] = sel4(av[i], q);
+#pragma unroll
+            for (int kk = 0; kk < 4; kk += 2) {
+                const int k0 = q * 4 + kk;
+                uint32_t a0[TM], a1[TM];  // byte address of row a of the b-major table: base + 2a
 #pragma unroll
                 for (int i = 0; i < TM; ++i) {
-                    const uint32_t w = sel4(av[i], q);
-                    a0[i] = __byte_perm(w, 0, s0);
-                    a1[i] = __byte_perm(w, 0, s0 + 1);
+                    a0[i] = __byte_perm(aw[i], 0, 0x4440u + kk) * 2u + lut_base;
+                    a1[i] = __byte_perm(aw[i], 0, 0x4441u + kk) * 2u + lut_base;
                 }
-                const uint4 w0a = *reinterpret_cast<const uint4 *>(ws + (2 * kp) * BN * 2);
-                const uint4 w0b = *reinterpret_cast<const uint4 *>(ws + (2 * kp) * BN * 2 + 16);
-                const uint4 w1a = *reinterpret_cast<const uint4 *>(ws + (2 * kp + 1) * BN * 2);
-                const uint4 w1b = *reinterpret_cast<const uint4 *>(ws + (2 * kp + 1) * BN * 2 + 16);
+                uint4 wv0[WG], wv1[WG];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint32_t sel = (j & 1) ? 0x4324u : 0x4104u;  // u16 half -> bytes 1..2 (= 2b << 8)
-                    const uint32_t b0 =
-                        __byte_perm(sel4(j < 8 ? w0a : w0b, (j >> 1) & 3), 0, sel) + lut_base;
-                    const uint32_t b1 =
-                        __byte_perm(sel4(j < 8 ? w1a : w1b, (j >> 1) & 3), 0, sel) + lut_base;
+                for (int g = 0; g < WG; ++g) {
+                    wv0[g] = *reinterpret_cast<const uint4 *>(ws + k0 * BN * 2 + g * 16);
+                    wv1[g] = *reinterpret_cast<const uint4 *>(ws + (k0 + 1) * BN * 2 + g * 16);
+                }
+#pragma unroll
+                for (int j = 0; j < TN; ++j) {
+                    // u16 (2b) -> bytes 1..2: (2b) << 8 = b << 9 = byte offset of row b
+                    const uint32_t sel = (j & 1) ? 0x4324u : 0x4104u;
+                    const uint32_t b0 = __byte_perm(sel4(wv0[j >> 3], (j >> 1) & 3), 0, sel);
+                    const uint32_t b1 = __byte_perm(sel4(wv1[j >> 3], (j >> 1) & 3), 0, sel);
 #pragma unroll
                     for (int i = 0; i < TM; ++i) {
                         int32_t v0, v1;
-                        const uint32_t ad0 = a0[i] * 2u + b0;
-                        const uint32_t ad1 = a1[i] * 2u + b1;
                         if (SGN) {
-                            asm("ld.shared.s16 %0, [%1];" : "=r"(v0) : "r"(ad0));
-                            asm("ld.shared.s16 %0, [%1];" : "=r"(v1) : "r"(ad1));
+                            asm("ld.shared.s16 %0, [%1];" : "=r"(v0) : "r"(a0[i] + b0));
+                            asm("ld.shared.s16 %0, [%1];" : "=r"(v1) : "r"(a1[i] + b1));
                         } else {
-                            asm("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(ad0));
-                            asm("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(ad1));
+                            asm("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0[i] + b0));
+                            asm("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1[i] + b1));
                         }
                         acc[i][j] += v0 + v1;
                     }
                 }
             }
         }
-        cp_async_wait<0>();
-        __syncthreads();  // stages are free for the next tile's prologue
 
-        // ------------------------------------------------ fused epilogue
+        if (++c_kc < p.nchunks) continue;
+        // ------------------------------------------------ fused epilogue for tile c_tile
+        c_kc = 0;
+        const int64_t m0 = (c_tile / p.ntn) * BM;
+        const int n0 = (int)(c_tile % p.ntn) * BN;
+        c_tile += gridDim.x;
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
             const int64_t m = m0 + wm * 32 * TM + i * 32 + lane;
-            if (m >= p.M) continue;
-            const int64_t sp = patch_sum(p, m, tappix_s);
-            psum_ovf |= (sp > INT32_MAX || sp < INT32_MIN);
-            float y[16];
+            if (m < p.M) {
+                const int64_t sp = patch_sum(p, m, tappix_s);
+                psum_ovf |= (sp > INT32_MAX || sp < INT32_MIN);
+                float y[TN];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int c = n0 + wn * 16 + j;
-                if (c < p.cout) {
-                    int64_t A;
-                    if (p.acc_mode == AXB_ACC_WRAP32) {
-                        A = (int64_t)(int32_t)((uint32_t)acc[i][j] - (uint32_t)e.junk);
-                    } else {
-                        A = (int64_t)acc[i][j] - e.junk;
-                        if (p.acc_mode == AXB_ACC_SATURATE32) A = A > INT32_MAX ? INT32_MAX : (A < INT32_MIN ? INT32_MIN : A);
+                for (int j = 0; j < TN; ++j) {
+                    const int c = n0 + wn * TN + j;
+                    y[j] = 0.0f;
+                    if (c < p.cout) {
+                        int64_t A;
+                        if (p.acc_mode == AXB_ACC_WRAP32) {
+                            A = (int64_t)(int32_t)((uint32_t)acc[i][j] - (uint32_t)e.junk);
+                        } else {
+                            A = (int64_t)acc[i][j] - e.junk;
+                            if (p.acc_mode == AXB_ACC_SATURATE32)
+                                A = A > INT32_MAX ? INT32_MAX : (A < INT32_MIN ? INT32_MIN : A);
+                        }
+                        if (p.acc_out) p.acc_out[m * p.cout + c] = A;
+                        y[j] = finish(p, e, A, sp, m, c);
+                        track(y[j], tmin, tmax, nonfinite);
                     }
-                    if (p.acc_out) p.acc_out[m * p.cout + c] = A;
-                    y[j] = finish(p, e, A, sp, m, c);
-                    track(y[j], tmin, tmax, nonfinite);
+                }
+                const int cb = n0 + wn * TN;
+                float *dst = p.out + m * p.cout + cb;
+                if (cb + TN <= p.cout && (p.cout & 3) == 0) {
+#pragma unroll
+                    for (int j = 0; j < TN; j += 4)
+                        *reinterpret_cast<float4 *>(dst + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < TN; ++j)
+                        if (cb + j < p.cout) dst[j] = y[j];
                 }
             }
-            const int cb = n0 + wn * 16;
-            float *dst = p.out + m * p.cout + cb;
-            if (cb + 16 <= p.cout && (p.cout & 3) == 0) {
 #pragma unroll
-                for (int j = 0; j < 16; j += 4)
-                    *reinterpret_cast<float4 *>(dst + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (cb + j < p.cout) dst[j] = y[j];
-            }
+            for (int j = 0; j < TN; ++j) acc[i][j] = 0;
         }
     }
-    if (!lut_ready) mbar_wait(bar, 0);  // never leave a bulk copy in flight at exit
+    cp_async_wait<0>();
     range_commit(tmin, tmax, nonfinite, p.out_range, p.flags, AXB_FLAG_OUT_NONFINITE);
     if (psum_ovf) atomicOr(p.flags, AXB_FLAG_PSUM_OVF);
 }
@@ -420,16 +429,32 @@ __global__ void __launch_bounds__(256) lutconv_generic(const ConvK p) {
 }
 
 // ---------------------------------------------------------------- host launch
-template <int TM, int WM, int WN, bool SGN, int SEG>
+struct Variant {
+    const char *name;
+    int tm, tn, wm, wn;
+};
+// tuning table (axb_conv_desc.variant selects one explicitly; 0 = heuristic)
+static const Variant kVariants[] = {
+    {"auto", 0, 0, 0, 0},
+    {"tm4tn16_w8x1", 4, 16, 8, 1},  {"tm4tn16_w4x2", 4, 16, 4, 2},  {"tm4tn16_w2x4", 4, 16, 2, 4},
+    {"tm4tn8_w8x2", 4, 8, 8, 2},    {"tm4tn8_w4x4", 4, 8, 4, 4},    {"tm4tn8_w16x1", 4, 8, 16, 1},
+    {"tm4tn16_w12x1", 4, 16, 12, 1}, {"tm4tn16_w6x2", 4, 16, 6, 2}, {"tm4tn16_w3x4", 4, 16, 3, 4},
+    {"tm2tn16_w16x1", 2, 16, 16, 1}, {"tm2tn16_w8x2", 2, 16, 8, 2}, {"tm4tn16_w4x4", 4, 16, 4, 4},
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+template <int TM, int TN, int WM, int WN, bool SGN>
 static int launch_fast(const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
-    constexpr int BM = WM * 32 * TM, BN = WN * 16;
+    constexpr int BM = WM * 32 * TM, BN = WN * TN;
     const size_t smem = kLutBytes + kStages * (BM * 16 + 16 * BN * 2) + 2 * kMaxTaps * 4 + 16;
-    auto fn = lutconv_fast<TM, WM, WN, SGN, SEG>;
-    static bool configured = false;  // one per instantiation
-    if (!configured) {
+    auto fn = lutconv_fast<TM, TN, WM, WN, SGN>;
+    static int configured_dev = -1;  // one per instantiation
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_fast");
-        configured = true;
+        configured_dev = dev;
     }
     ConvK kk = k;
     kk.ntn = (k.coutp + BN - 1) / BN;
@@ -437,16 +462,35 @@ static int launch_fast(const ConvK &k, int sm_limit, cudaStream_t s, const char 
     int64_t grid = sm_limit > 0 ? sm_limit : sm_count();
     if (grid > kk.ntiles) grid = kk.ntiles;
     if (grid < 1) grid = 1;
-    fn<<<(int)grid, kThreads, smem, s>>>(kk);
+    fn<<<(int)grid, WM * WN * 32, smem, s>>>(kk);
     set_last_kernel(name);
     return check_launch("lutconv_fast");
 }
 
-template <bool SGN, int SEG>
-static int dispatch_tile(const ConvK &k, int sm_limit, cudaStream_t s) {
-    if (k.coutp <= 16) return launch_fast<4, 8, 1, SGN, SEG>(k, sm_limit, s, "lutconv_fast<TM4,8x1>");
-    if (k.coutp <= 32) return launch_fast<4, 4, 2, SGN, SEG>(k, sm_limit, s, "lutconv_fast<TM4,4x2>");
-    return launch_fast<4, 2, 4, SGN, SEG>(k, sm_limit, s, "lutconv_fast<TM4,2x4>");
+template <bool SGN>
+static int launch_variant(int v, const ConvK &k, int sm_limit, cudaStream_t s) {
+    const char *nm = kVariants[v].name;
+    switch (v) {
+        case 1: return launch_fast<4, 16, 8, 1, SGN>(k, sm_limit, s, nm);
+        case 2: return launch_fast<4, 16, 4, 2, SGN>(k, sm_limit, s, nm);
+        case 3: return launch_fast<4, 16, 2, 4, SGN>(k, sm_limit, s, nm);
+        case 4: return launch_fast<4, 8, 8, 2, SGN>(k, sm_limit, s, nm);
+        case 5: return launch_fast<4, 8, 4, 4, SGN>(k, sm_limit, s, nm);
+        case 6: return launch_fast<4, 8, 16, 1, SGN>(k, sm_limit, s, nm);
+        case 7: return launch_fast<4, 16, 12, 1, SGN>(k, sm_limit, s, nm);
+        case 8: return launch_fast<4, 16, 6, 2, SGN>(k, sm_limit, s, nm);
+        case 9: return launch_fast<4, 16, 3, 4, SGN>(k, sm_limit, s, nm);
+        case 10: return launch_fast<2, 16, 16, 1, SGN>(k, sm_limit, s, nm);
+        case 11: return launch_fast<2, 16, 8, 2, SGN>(k, sm_limit, s, nm);
+        case 12: return launch_fast<4, 16, 4, 4, SGN>(k, sm_limit, s, nm);
+        default: return set_error(AXB_E_VALUE, "unknown conv kernel variant");
+    }
+}
+
+static int pick_variant(const ConvK &k) {
+    if (k.coutp <= 16) return 1;
+    if (k.coutp <= 32) return 2;
+    return 3;
 }
 
 }  // namespace axb
@@ -494,14 +538,31 @@ int axb_conv2d_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
     k.f00 = lut->f00;
     cudaStream_t s = (cudaStream_t)stream;
 
-    const int64_t code_bytes = d->n * d->hp * d->wp * d->cs;
-    const bool fast = !d->force_generic && d->kpad <= 32768 && k.taps <= kMaxTaps &&
-                      (d->cs == 4 || d->cs % 16 == 0) && code_bytes < (int64_t(1) << 31) &&
+    const bool fast = !d->force_generic && d->kpad <= 32768 && k.taps <= kMaxTaps && d->cs % 16 == 0 &&
                       d->kpad % 16 == 0 && d->coutp % 16 == 0;
     if (fast) {
-        if (lut->is_signed)
-            return d->cs == 4 ? dispatch_tile<true, 4>(k, d->sm_limit, s) : dispatch_tile<true, 16>(k, d->sm_limit, s);
-        return d->cs == 4 ? dispatch_tile<false, 4>(k, d->sm_limit, s) : dispatch_tile<false, 16>(k, d->sm_limit, s);
+        int v = d->variant;
+        if (v < 0 || v >= kNumVariants) return set_error(AXB_E_VALUE, "unknown conv kernel variant");
+        if (v == 0) v = pick_variant(k);
+        // int32 gather offsets: split the batch so every launch's code tensor stays < 2 GiB
+        const int64_t per_img = d->hp * d->wp * d->cs;
+        int64_t step = ((int64_t(1) << 31) - 1) / (per_img > 0 ? per_img : 1);
+        if (step < 1) return set_error(AXB_E_VALUE, "one image's code tensor exceeds 2 GiB");
+        for (int64_t b0 = 0; b0 < d->n; b0 += step) {
+            const int64_t nb = (d->n - b0 < step) ? d->n - b0 : step;
+            ConvK kc = k;
+            kc.codes = d->codes + b0 * per_img;
+            kc.pixsum = d->pixsum + b0 * d->hp * d->wp;
+            kc.M = nb * d->oh * d->ow;
+            const int64_t ooff = b0 * d->oh * d->ow * d->cout;
+            kc.out = d->out + ooff;
+            kc.residual = d->residual ? d->residual + ooff : nullptr;
+            kc.acc_out = d->acc_out ? d->acc_out + ooff : nullptr;
+            const int rc = lut->is_signed ? launch_variant<true>(v, kc, d->sm_limit, s)
+                                          : launch_variant<false>(v, kc, d->sm_limit, s);
+            if (rc) return rc;
+        }
+        return AXB_OK;
     }
     int64_t blocks = (M * d->cout + 255) / 256;
     const int64_t cap = (int64_t)sm_count() * 32;
@@ -513,5 +574,8 @@ int axb_conv2d_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
     set_last_kernel("lutconv_generic");
     return check_launch("lutconv_generic");
 }
+
+int axb_conv_variant_count(void) { return kNumVariants; }
+const char *axb_conv_variant_name(int v) { return (v >= 0 && v < kNumVariants) ? kVariants[v].name : ""; }
 
 }  // extern "C"

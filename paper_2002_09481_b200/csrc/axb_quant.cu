@@ -230,6 +230,49 @@ __global__ void filters_sum_kernel(const uint16_t *__restrict__ fcodes, int64_t 
     }
 }
 
+// ---------------------------------------------------------------- im2col of codes
+// One thread per output row: gathers the kh*kw*c codes of its window from the
+// zp-padded code tensor into kp/16 16-byte pieces (zeros beyond K) and writes
+// the exact row sum (= patch sum S_p, axconv.py:193).
+__global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t *__restrict__ codes, int64_t n, int64_t hp,
+                                                          int64_t wp, int64_t cs, int c, int kh, int kw, int sh,
+                                                          int sw, int dh, int dw, int64_t oh, int64_t ow, int kp,
+                                                          int is_signed, uint8_t *__restrict__ rows,
+                                                          int32_t *__restrict__ rowsum) {
+    const int64_t total = n * oh * ow;
+    const int K = kh * kw * c;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < total;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = r % ow;
+        const int64_t t = r / ow;
+        const int64_t oy = t % oh;
+        const int64_t b = t / oh;
+        const uint8_t *base = codes + ((b * hp + oy * sh) * wp + ox * sw) * cs;
+        int32_t s = 0;
+        int k = 0, ky = 0, kx = 0, ci = 0;
+        for (int g = 0; g < kp / 16; ++g) {
+            uint32_t wv[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int u = 0; u < 16; ++u, ++k) {
+                if (k < K) {
+                    const uint32_t byte = base[((int64_t)ky * dh * wp + kx * dw) * cs + ci];
+                    s += is_signed ? (int32_t)(int8_t)byte : (int32_t)byte;
+                    wv[u >> 2] |= byte << (8 * (u & 3));
+                    if (++ci == c) {
+                        ci = 0;
+                        if (++kx == kw) {
+                            kx = 0;
+                            ++ky;
+                        }
+                    }
+                }
+            }
+            reinterpret_cast<uint4 *>(rows + r * kp)[g] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        rowsum[r] = s;
+    }
+}
+
 }  // namespace axb
 
 // ======================================================================== C ABI
@@ -237,9 +280,26 @@ using namespace axb;
 
 extern "C" {
 
-int64_t axb_channel_stride(int64_t c) {
-    if (c <= 4) return 4;
-    return (c + 15) / 16 * 16;
+int64_t axb_channel_stride(int64_t c) { return (c + 15) / 16 * 16; }
+
+int64_t axb_conv_im2col_kp(int64_t c, int64_t kh, int64_t kw) {
+    if (c % 16 == 0 || kh * kw == 1) return 0;
+    return (kh * kw * c + 15) / 16 * 16;
+}
+
+int axb_im2col_pack(const uint8_t *d_codes, int64_t n, int64_t hp, int64_t wp, int64_t cs, int64_t c, int32_t kh,
+                    int32_t kw, int32_t sh, int32_t sw, int32_t dh, int32_t dw, int64_t oh, int64_t ow, int64_t kp,
+                    int is_signed, uint8_t *d_rows, int32_t *d_rowsum, void *stream) {
+    const int64_t rows = n * oh * ow;
+    if (rows == 0) return AXB_OK;
+    if (kp % 16 || kp < kh * kw * c) return set_error(AXB_E_VALUE, "bad im2col row length");
+    int64_t blocks = (rows + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    im2col_pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_codes, n, hp, wp, cs, (int)c, kh, kw, sh, sw,
+                                                                       dh, dw, oh, ow, (int)kp, is_signed, d_rows,
+                                                                       d_rowsum);
+    return check_launch("im2col_pack");
 }
 
 int axb_range_reset(int32_t *d_range, void *stream) {
@@ -304,12 +364,8 @@ int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t 
     if (cs <= 16) {
         int64_t blocks = (total + 255) / 256;
         if (blocks > cap) blocks = cap;
-        if (cs == 4)
-            quantize_pad_small<4><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, pt, pl, hp, wp, d_params,
-                                                              is_signed, round_mode, d_codes, d_pixsum, d_flags);
-        else
-            quantize_pad_small<16><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, pt, pl, hp, wp, d_params,
-                                                               is_signed, round_mode, d_codes, d_pixsum, d_flags);
+        quantize_pad_small<16><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, pt, pl, hp, wp, d_params,
+                                                           is_signed, round_mode, d_codes, d_pixsum, d_flags);
     } else {
         int64_t blocks = (total * 32 + 255) / 256;
         if (blocks > cap) blocks = cap;

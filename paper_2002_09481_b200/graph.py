@@ -32,8 +32,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .axconv import device_lut
-from .types import ConvGeometry, _mode_value, is_signed, output_shape, resolve_padding
+from .layer import ConvLayer
+from .types import ConvGeometry, _mode_value, output_shape, resolve_padding
 
 _I32_MAX = 2**31 - 1
 _I32_MIN = -(2**31)
@@ -65,18 +65,7 @@ class _ConvPlan:
     in_shape: tuple = ()
     out_shape: tuple = ()
     pads: tuple = ()
-    kh: int = 0
-    kw: int = 0
-    cin: int = 0
-    cout: int = 0
-    cs: int = 0
-    kpad: int = 0
-    coutp: int = 0
-    lut: object = None
-    fcodes: torch.Tensor = None
-    fsum: torch.Tensor = None
-    bias: torch.Tensor | None = None
-    params: torch.Tensor = None  # [in, f] axb_qparams as 2 x 16 bytes
+    layer: ConvLayer | None = None
 
 
 @dataclass
@@ -91,14 +80,17 @@ class GpuGraph:
     """Prepared graph: filters quantized once (hoisted, cf. axconv.py:287), fusion planned."""
 
     def __init__(self, nodes, device=None, accumulator="exact64", round_mode="half-away-from-zero",
-                 in_shape=None, sm_limit: int = 0):
+                 in_shape=None, sm_limit: int = 0, variant: int = 0):
         if not torch.cuda.is_available():
             raise _lib.AxbError("GpuGraph needs a CUDA device (no CPU fallback)")
         self.nodes = list(nodes)
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
-        self.acc = _lib.ACC[_mode_value(accumulator)]
-        self.round = _lib.ROUND[_mode_value(round_mode)]
+        self.acc_name = _mode_value(accumulator)
+        self.round_name = _mode_value(round_mode)
+        self.acc = _lib.ACC[self.acc_name]
+        self.round = _lib.ROUND[self.round_name]
         self.sm_limit = int(sm_limit)
+        self.variant = int(variant)
         self.lib = _lib.load()
         self._plan()
 
@@ -210,11 +202,10 @@ class GpuGraph:
                 p.geometry = _geometry(a)
                 p.in_shape = xs
                 p.out_shape = output_shape(xs, f.shape, p.geometry)
-                p.kh, p.kw, p.cin, p.cout = (int(v) for v in f.shape)
-                p.pads = resolve_padding(p.geometry, xs[1], xs[2], p.kh, p.kw)
                 shapes[n["id"]] = p.out_shape
-                if p.fcodes is None:
-                    self._prepare_filters(p, a)
+                if p.layer is None:
+                    p.layer = ConvLayer(f, (a["f_min"], a["f_max"]), a["lut"], p.geometry, a.get("bias"),
+                                        self.round_name, self.acc_name, self.device.index)
             elif st.kind in ("ReLU", "Add"):
                 shapes[n["id"]] = shapes[self.t(n["inputs"][0])]
             elif st.kind in ("MaxPool", "AvgPool"):
@@ -233,33 +224,6 @@ class GpuGraph:
                 shapes[n["id"]] = shapes[self.t(n["inputs"][0])]
         self.shapes = shapes
         self._prepared_for = tuple(in_shape)
-
-    def _prepare_filters(self, p: _ConvPlan, a):
-        lib = self.lib
-        p.lut = device_lut(a["lut"], self.device.index)
-        sgn = int(p.lut.signed)
-        p.cs = int(lib.axb_channel_stride(p.cin))
-        p.kpad = int(lib.axb_filter_kpad(p.kh, p.kw, p.cs))
-        p.coutp = int(lib.axb_filter_coutp(p.cout))
-        f = torch.from_numpy(np.ascontiguousarray(a["filters"], dtype=np.float32)).to(self.device)
-        p.params = torch.zeros(2, 16, dtype=torch.uint8, device=self.device)
-        hp = _lib.QParams()
-        _lib.check(lib.axb_coeffs_host(float(a["f_min"]), float(a["f_max"]), sgn, self.round, hp))
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(lib.axb_params_upload(hp, p.params[1].data_ptr(), stream))
-        p.fcodes = torch.empty(p.kpad * p.coutp, dtype=torch.int16, device=self.device)
-        p.fsum = torch.empty(max(p.cout, 1), dtype=torch.int64, device=self.device)
-        fl = torch.zeros(1, dtype=torch.int32, device=self.device)
-        _lib.check(lib.axb_filters_prepare(f.data_ptr(), p.kh, p.kw, p.cin, p.cout, p.cs, p.params[1].data_ptr(),
-                                           sgn, self.round, p.fcodes.data_ptr(), p.fsum.data_ptr(),
-                                           fl.data_ptr(), stream))
-        flags = int(fl.item())
-        if flags & _lib.FLAG_NONFINITE:
-            raise ValueError("cannot quantize non-finite values")
-        if flags & _lib.FLAG_FSUM_OVF:
-            raise OverflowError("filter size too large for 32-bit code sums")
-        b = a.get("bias")
-        p.bias = None if b is None else torch.from_numpy(np.ascontiguousarray(b, np.float32)).to(self.device)
 
     # ------------------------------------------------------------------ execution
     def run(self, batch: torch.Tensor, check: bool = True, trace: dict | None = None,
@@ -379,54 +343,15 @@ class GpuGraph:
                     raise OverflowError("patch length too large for 32-bit code sums")
 
     def _run_conv(self, p: _ConvPlan, vals, out_range, out_flag, stream):
-        lib = self.lib
         x = vals[self.t(p.x)]
-        n, h, w, c = p.in_shape
-        _, oh, ow, cout = p.out_shape
-        out = torch.empty(p.out_shape, dtype=torch.float32, device=self.device)
-        if n == 0:
-            return out
-        sgn = int(p.lut.signed)
-        pt, pb, pl, pr = p.pads
-        hp, wp = h + pt + pb, w + pl + pr
-        codes = torch.empty(n * hp * wp * p.cs, dtype=torch.uint8, device=self.device)
-        pixsum = torch.empty(n * hp * wp, dtype=torch.int32, device=self.device)
-        xr = self.ranges[self.slot[self.t(p.x)]].data_ptr()
-        _lib.check(lib.axb_coeffs_from_range(xr, sgn, self.round, p.params[0].data_ptr(), stream))
-        qflag = self.flags[len(self.slot)].data_ptr()
-        _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, p.cs, p.params[0].data_ptr(),
-                                        sgn, self.round, codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
-        d = _lib.ConvDesc()
-        d.codes, d.pixsum = codes.data_ptr(), pixsum.data_ptr()
-        d.n, d.hp, d.wp, d.cs, d.c = n, hp, wp, p.cs, c
-        d.kh, d.kw = p.kh, p.kw
-        d.sh, d.sw = p.geometry.strides
-        d.dh, d.dw = p.geometry.dilations
-        d.oh, d.ow = oh, ow
-        d.fcodes, d.fsum = p.fcodes.data_ptr(), p.fsum.data_ptr()
-        d.cout, d.coutp, d.kpad = cout, p.coutp, p.kpad
-        d.in_params, d.f_params = p.params[0].data_ptr(), p.params[1].data_ptr()
-        d.accumulator = self.acc
-        d.relu = int(p.relu)
-        d.bias = p.bias.data_ptr() if p.bias is not None else None
-        if p.residual is not None:
-            r = vals[self.t(p.residual)]
-            if tuple(r.shape) != tuple(p.out_shape):
-                raise ValueError(f"Add input shapes differ at {p.node['id']!r}")
-            d.residual = r.data_ptr()
-        d.out = out.data_ptr()
-        d.out_range = out_range
-        d.flags = out_flag
-        d.sm_limit = self.sm_limit
-        prof = self._profile
-        if prof is not None:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-        _lib.check(lib.axb_conv2d_lut(d, p.lut.handle, stream))
-        if prof is not None:
-            e1.record()
-            prof.append((p.node["id"], e0, e1, n * oh * ow * p.kh * p.kw * c * cout))
-        self.launches += 3  # coeffs, quantize, conv
+        res = vals[self.t(p.residual)] if p.residual is not None else None
+        prof = [] if self._profile is not None else None
+        out = p.layer.run(x, self.ranges[self.slot[self.t(p.x)]].data_ptr(), relu=p.relu, residual=res,
+                          out_range=out_range, out_flag=out_flag, quant_flag=self.flags[len(self.slot)].data_ptr(),
+                          sm_limit=self.sm_limit, variant=self.variant, profile=prof)
+        if prof:
+            self._profile.append((p.node["id"],) + prof[0])
+        self.launches += p.layer.launches
         return out
 
 

@@ -1,0 +1,150 @@
+"""One prepared approximate-conv layer on one device (the per-node unit of the executor).
+
+Filters are quantized once at construction (the reference re-quantizes them
+on every call, axconv.py:287; hoisting is bit-neutral because the filter
+range is a constant, graph.py:129-130).  ``run`` executes, stream-ordered:
+
+  coefficients of the input range (device, no sync)      quantizer.py:98-117
+  K2 quantize + zero-point pad                             quantizer.py:120-131, axconv.py:181-189
+  [im2col of the codes, small-channel layers only]         axconv.py:160-196
+  K3 LUT implicit GEMM + fused epilogue                    axconv.py:136-146, :246-256, graph.py:268-286
+
+Path choice (``libaxb``): channels are padded to a multiple of 16 (raw-0
+codes whose exact contribution the epilogue removes); when that padding would
+waste lookups (c % 16 != 0 with a multi-tap kernel, e.g. the RGB stem) the
+codes are gathered into dense kp = roundup16(kh*kw*c) rows and the conv runs
+as a 1x1 over them.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .axconv import device_lut
+from .types import resolve_padding
+
+
+class ConvLayer:
+    def __init__(self, filters, f_range, lut, geometry, bias=None, round_mode="half-away-from-zero",
+                 accumulator="exact64", device=None):
+        self.lib = lib = _lib.load()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        f = np.ascontiguousarray(filters, dtype=np.float32)
+        self.kh, self.kw, self.cin, self.cout = (int(v) for v in f.shape)
+        self.geometry = geometry
+        self.round = _lib.ROUND[getattr(round_mode, "value", round_mode)]
+        self.acc = _lib.ACC[getattr(accumulator, "value", accumulator)]
+        self.lut = device_lut(lut, self.device.index)
+        self.sgn = int(self.lut.signed)
+        self.cs = int(lib.axb_channel_stride(self.cin))
+        self.kp = int(lib.axb_conv_im2col_kp(self.cin, self.kh, self.kw))
+        if self.kp:  # filters as (1, 1, K, cout): same (ky, kx, ci) flattening
+            fk = (1, 1, self.kh * self.kw * self.cin, self.kp)
+        else:
+            fk = (self.kh, self.kw, self.cin, self.cs)
+        self.f_geom = fk
+        self.kpad = int(lib.axb_filter_kpad(fk[0], fk[1], fk[3]))
+        self.coutp = int(lib.axb_filter_coutp(self.cout))
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.params = torch.zeros(2, 16, dtype=torch.uint8, device=self.device)  # [input, filter] axb_qparams
+        hp = _lib.QParams()
+        _lib.check(lib.axb_coeffs_host(float(f_range[0]), float(f_range[1]), self.sgn, self.round, hp))
+        _lib.check(lib.axb_params_upload(hp, self.params[1].data_ptr(), stream))
+        fd = torch.from_numpy(f).to(self.device)
+        self.fcodes = torch.empty(self.kpad * self.coutp, dtype=torch.int16, device=self.device)
+        self.fsum = torch.empty(max(self.cout, 1), dtype=torch.int64, device=self.device)
+        fl = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _lib.check(lib.axb_filters_prepare(fd.data_ptr(), fk[0], fk[1], fk[2], self.cout, fk[3],
+                                           self.params[1].data_ptr(), self.sgn, self.round, self.fcodes.data_ptr(),
+                                           self.fsum.data_ptr(), fl.data_ptr(), stream))
+        flags = int(fl.item())
+        if flags & _lib.FLAG_NONFINITE:
+            raise ValueError("cannot quantize non-finite values")
+        if flags & _lib.FLAG_FSUM_OVF:
+            raise OverflowError("filter size too large for 32-bit code sums")
+        self.bias = None if bias is None else torch.from_numpy(np.ascontiguousarray(bias, np.float32)).to(self.device)
+        self.launches = 0
+
+    def set_input_params(self, mn: float, mx: float) -> None:
+        """Host range (the operator-API path): coefficients computed on the host, uploaded."""
+        hp = _lib.QParams()
+        _lib.check(self.lib.axb_coeffs_host(float(mn), float(mx), self.sgn, self.round, hp))
+        _lib.check(self.lib.axb_params_upload(hp, self.params[0].data_ptr(),
+                                              torch.cuda.current_stream(self.device).cuda_stream))
+
+    def run(self, x: torch.Tensor, in_range_dev=None, *, relu=False, residual=None, out_range=None,
+            out_flag=None, quant_flag=None, acc_out=None, force_generic=False, sm_limit=0, variant=0,
+            profile=None) -> torch.Tensor:
+        """x: (n,h,w,cin) fp32 CUDA.  in_range_dev: device int32[2] ordered-float range, or None if
+        set_input_params() was called.  Returns (n,oh,ow,cout) fp32."""
+        lib = self.lib
+        n, h, w, c = (int(v) for v in x.shape)
+        if c != self.cin:
+            raise ValueError(f"filter channels {self.cin} do not match input channels {c}")
+        g = self.geometry
+        pt, pb, pl, pr = resolve_padding(g, h, w, self.kh, self.kw)
+        hp_, wp_ = h + pt + pb, w + pl + pr
+        ekh, ekw = (self.kh - 1) * g.dilations[0] + 1, (self.kw - 1) * g.dilations[1] + 1
+        if hp_ < ekh or wp_ < ekw:
+            raise ValueError(f"kernel extent {max(ekh, ekw)} exceeds padded input")
+        oh, ow = (hp_ - ekh) // g.strides[0] + 1, (wp_ - ekw) // g.strides[1] + 1
+        out = torch.empty((n, oh, ow, self.cout), dtype=torch.float32, device=self.device)
+        if n == 0 or self.cout == 0:
+            return out
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.launches = 0
+        if in_range_dev is not None:
+            _lib.check(lib.axb_coeffs_from_range(in_range_dev, self.sgn, self.round, self.params[0].data_ptr(), stream))
+            self.launches += 1
+        qflag = quant_flag if quant_flag is not None else out_flag
+        codes = torch.empty(n * hp_ * wp_ * self.cs, dtype=torch.uint8, device=self.device)
+        pixsum = torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
+        _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, self.cs, self.params[0].data_ptr(),
+                                        self.sgn, self.round, codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
+        self.launches += 1
+        d = _lib.ConvDesc()
+        if self.kp:
+            rows = torch.empty(n * oh * ow * self.kp, dtype=torch.uint8, device=self.device)
+            rsum = torch.empty(n * oh * ow, dtype=torch.int32, device=self.device)
+            _lib.check(lib.axb_im2col_pack(codes.data_ptr(), n, hp_, wp_, self.cs, c, self.kh, self.kw,
+                                           g.strides[0], g.strides[1], g.dilations[0], g.dilations[1], oh, ow,
+                                           self.kp, self.sgn, rows.data_ptr(), rsum.data_ptr(), stream))
+            self.launches += 1
+            codes, pixsum = rows, rsum
+            d.n, d.hp, d.wp, d.cs, d.c = n, oh, ow, self.kp, self.kh * self.kw * c
+            d.kh = d.kw = d.sh = d.sw = d.dh = d.dw = 1
+        else:
+            d.n, d.hp, d.wp, d.cs, d.c = n, hp_, wp_, self.cs, c
+            d.kh, d.kw = self.kh, self.kw
+            d.sh, d.sw = g.strides
+            d.dh, d.dw = g.dilations
+        d.codes, d.pixsum = codes.data_ptr(), pixsum.data_ptr()
+        d.oh, d.ow = oh, ow
+        d.fcodes, d.fsum = self.fcodes.data_ptr(), self.fsum.data_ptr()
+        d.cout, d.coutp, d.kpad = self.cout, self.coutp, self.kpad
+        d.in_params, d.f_params = self.params[0].data_ptr(), self.params[1].data_ptr()
+        d.accumulator = self.acc
+        d.relu = int(relu)
+        d.bias = self.bias.data_ptr() if self.bias is not None else None
+        if residual is not None:
+            if tuple(residual.shape) != tuple(out.shape):
+                raise ValueError("Add input shapes differ")
+            d.residual = residual.data_ptr()
+        d.out = out.data_ptr()
+        d.acc_out = acc_out.data_ptr() if acc_out is not None else None
+        d.out_range = out_range
+        d.flags = out_flag
+        d.force_generic = int(force_generic)
+        d.sm_limit = int(sm_limit)
+        d.variant = int(variant)
+        if profile is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        _lib.check(lib.axb_conv2d_lut(d, self.lut.handle, stream))
+        self.launches += 1
+        if profile is not None:
+            e1.record()
+            profile.append((e0, e1, n * oh * ow * self.kh * self.kw * c * self.cout))
+        return out

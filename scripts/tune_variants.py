@@ -1,0 +1,87 @@
+"""Time every fast-kernel tile variant on the real per-layer inputs of a workload.
+
+    python scripts/tune_variants.py --workload r8 [--out gpurun_out/tune_r8.json]
+
+Runs the graph once with a trace to capture each conv's actual input tensor,
+then re-runs every AxConv2D layer alone with each variant (CUDA events, median
+of 5) and checks the outputs are bit-identical across variants.
+"""
+
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from bench import make_images, workload_spec  # noqa: E402
+from paper_2002_09481_b200 import _lib  # noqa: E402
+from paper_2002_09481_b200.graph import GpuGraph, _geometry  # noqa: E402
+from paper_2002_09481_b200.layer import ConvLayer  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="r8")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--out", default="")
+    ap.add_argument("--variants", default="")
+    args = ap.parse_args()
+    spec = workload_spec(args.workload, "trunc2")
+    batch = args.batch or spec["batch"]
+    imgs, _ = make_images(spec["kind"], batch, seed=1000)
+    g = GpuGraph(spec["nodes"])
+    trace = {}
+    g.run(torch.from_numpy(imgs).cuda(), trace=trace)
+    nvar = _lib.load().axb_conv_variant_count()
+    variants = [int(v) for v in args.variants.split(",")] if args.variants else list(range(1, nvar))
+    names = [_lib.load().axb_conv_variant_name(v).decode() for v in range(nvar)]
+    rows = []
+    seen = set()
+    for n in spec["nodes"]:
+        if n["kind"] != "AxConv2D":
+            continue
+        a = n["attrs"]
+        x = trace[n["inputs"][0]]
+        key = (tuple(x.shape), a["filters"].shape, tuple(a["strides"]))
+        if key in seen:
+            continue
+        seen.add(key)
+        layer = ConvLayer(a["filters"], (a["f_min"], a["f_max"]), a["lut"], _geometry(a), a.get("bias"))
+        layer.set_input_params(float(x.min()), float(x.max()))
+        flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+        res = {}
+        ref = None
+        for v in variants:
+            times = []
+            for _ in range(6):
+                prof = []
+                y = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(), variant=v,
+                              profile=prof)
+                e0, e1, macs = prof[0]
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            t = statistics.median(times[1:])
+            if ref is None:
+                ref = y
+            elif not torch.equal(ref.view(torch.int32), y.view(torch.int32)):
+                raise SystemExit(f"variant {names[v]} differs on {n['id']}")
+            res[names[v]] = round(t, 4)
+        best = min(res, key=res.get)
+        sm = torch.cuda.get_device_properties(0).multi_processor_count
+        peak = sm * 32 * 1.965e9
+        row = {"node": n["id"], "in": list(x.shape), "filters": list(a["filters"].shape), "macs": macs,
+               "best": best, "best_frac": round(macs / (res[best] / 1e3) / peak, 4), "ms": res}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(rows, indent=1))
+
+
+if __name__ == "__main__":
+    main()

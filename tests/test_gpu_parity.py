@@ -28,64 +28,27 @@ def _lut(entries, mode):
     return T.MultLut(T.Signedness(mode), np.asarray(entries).astype(T.Signedness(mode).entry_dtype))
 
 
-def gpu_conv(case, acc=True, force_generic=False, sm_limit=0):
-    """Run one case through the individual C-ABI stages (quantize, prepare, conv)."""
+def gpu_conv(case, acc=True, force_generic=False, sm_limit=0, variant=0):
+    """Run one case through ConvLayer (C-ABI stages: coeffs, quantize, [im2col], conv)."""
     torch = _torch()
     from paper_2002_09481_b200 import _lib
-    from paper_2002_09481_b200.axconv import device_lut
-    from paper_2002_09481_b200.types import ConvGeometry, output_shape, resolve_padding
+    from paper_2002_09481_b200.layer import ConvLayer
+    from paper_2002_09481_b200.types import ConvGeometry, output_shape
 
-    lib = _lib.load()
-    dev = torch.device("cuda")
-    x = torch.from_numpy(case["x"]).to(dev)
-    f = torch.from_numpy(case["f"]).to(dev)
-    n, h, w, c = case["x"].shape
-    kh, kw, _, cout = case["f"].shape
     geo = ConvGeometry(case["strides"], case["dilations"], case["padding"])
-    _, oh, ow, _ = output_shape(case["x"].shape, case["f"].shape, geo)
-    pt, pb, pl, pr = resolve_padding(geo, h, w, kh, kw)
-    sgn = int(case["mode"] == O.SIGNED)
-    rm = _lib.ROUND[case["round_mode"]]
-    dl = device_lut(_lut(case["lut"], case["mode"]))
-    s = torch.cuda.current_stream().cuda_stream
-    params = torch.zeros(2, 16, dtype=torch.uint8, device=dev)
-    for i, r in enumerate((case["in_range"], case["f_range"])):
-        hp_ = _lib.QParams()
-        _lib.check(lib.axb_coeffs_host(float(r[0]), float(r[1]), sgn, rm, hp_))
-        _lib.check(lib.axb_params_upload(hp_, params[i].data_ptr(), s))
-    cs = lib.axb_channel_stride(c)
-    kpad, coutp = lib.axb_filter_kpad(kh, kw, cs), lib.axb_filter_coutp(cout)
-    hp, wp = h + pt + pb, w + pl + pr
-    codes = torch.empty(n * hp * wp * cs, dtype=torch.uint8, device=dev)
-    pixsum = torch.empty(n * hp * wp, dtype=torch.int32, device=dev)
-    fcodes = torch.empty(kpad * coutp, dtype=torch.int16, device=dev)
-    fsum = torch.empty(cout, dtype=torch.int64, device=dev)
-    flags = torch.zeros(4, dtype=torch.int32, device=dev)
-    _lib.check(lib.axb_filters_prepare(f.data_ptr(), kh, kw, c, cout, cs, params[1].data_ptr(), sgn, rm,
-                                       fcodes.data_ptr(), fsum.data_ptr(), flags[0].data_ptr(), s))
-    _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, cs, params[0].data_ptr(), sgn, rm,
-                                    codes.data_ptr(), pixsum.data_ptr(), flags[1].data_ptr(), s))
-    out = torch.empty((n, oh, ow, cout), dtype=torch.float32, device=dev)
-    acc_out = torch.empty((n, oh, ow, cout), dtype=torch.int64, device=dev) if acc else None
-    d = _lib.ConvDesc()
-    d.codes, d.pixsum = codes.data_ptr(), pixsum.data_ptr()
-    d.n, d.hp, d.wp, d.cs, d.c = n, hp, wp, cs, c
-    d.kh, d.kw = kh, kw
-    d.sh, d.sw = geo.strides
-    d.dh, d.dw = geo.dilations
-    d.oh, d.ow = oh, ow
-    d.fcodes, d.fsum, d.cout, d.coutp, d.kpad = fcodes.data_ptr(), fsum.data_ptr(), cout, coutp, kpad
-    d.in_params, d.f_params = params[0].data_ptr(), params[1].data_ptr()
-    d.accumulator = _lib.ACC[case["accumulator"]]
-    d.out = out.data_ptr()
-    d.acc_out = acc_out.data_ptr() if acc else None
-    d.flags = flags[2].data_ptr()
-    d.force_generic = int(force_generic)
-    d.sm_limit = sm_limit
-    _lib.check(lib.axb_conv2d_lut(d, dl.handle, s))
+    layer = ConvLayer(case["f"], case["f_range"], _lut(case["lut"], case["mode"]), geo,
+                      round_mode=case["round_mode"], accumulator=case["accumulator"])
+    layer.set_input_params(*case["in_range"])
+    x = torch.from_numpy(case["x"]).cuda()
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    acc_t = None
+    if acc:
+        acc_t = torch.empty(output_shape(case["x"].shape, case["f"].shape, geo), dtype=torch.int64, device="cuda")
+    y = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(),
+                  force_generic=force_generic, sm_limit=sm_limit, variant=variant, acc_out=acc_t)
     torch.cuda.synchronize()
     kernel = _lib.last_kernel()
-    return out.cpu().numpy(), (acc_out.cpu().numpy() if acc else None), kernel
+    return y.cpu().numpy(), (acc_t.cpu().numpy() if acc else None), kernel
 
 
 @pytest.mark.parametrize("generic", [False, True])
@@ -99,7 +62,28 @@ def test_c1_cases_bit_exact(generic):
         kernels.add(kern.split("<")[0])
         assert bits_equal(y, g[f"out_{i}"]), (i, kern)
         assert np.array_equal(acc, g[f"acc_{i}"]), (i, kern)
-    assert kernels == ({"lutconv_generic"} if generic else {"lutconv_fast"})
+    assert kernels == ({"lutconv_generic"} if generic else {"tm4tn16_w8x1"})
+
+
+def test_all_tile_variants_bit_identical():
+    """Every fast-kernel tile variant (warps x pixels x channels) gives the same bits on seeded cases."""
+    from paper_2002_09481_b200 import _lib
+
+    nvar = _lib.load().axb_conv_variant_count()
+    rng = np.random.default_rng(77)
+    cases = [random_conv_case(rng) for _ in range(12)]
+    big = dict(x=np.maximum(rng.standard_normal((3, 17, 19, 48)), 0).astype(np.float32),
+               f=rng.standard_normal((3, 3, 48, 70)).astype(np.float32), lut=O.random_lut(rng, O.SIGNED),
+               mode=O.SIGNED, padding="same", strides=(1, 1), dilations=(1, 1), accumulator=O.EXACT64,
+               round_mode=O.HALF_EVEN)
+    big.update(in_range=(float(big["x"].min()), float(big["x"].max())),
+               f_range=(float(big["f"].min()), float(big["f"].max())))
+    for case in cases + [big]:
+        want, want_acc = oracle_conv(case, return_acc=True)
+        for v in range(1, nvar):
+            y, acc, kern = gpu_conv(case, variant=v)
+            assert bits_equal(y, want), (v, kern)
+            assert np.array_equal(acc, want_acc), (v, kern)
 
 
 def test_c1_through_operator_api():
@@ -340,7 +324,7 @@ def test_exact_lut_control_full_size_layer():
                     lut=O.exact_lut(mode), mode=mode, padding="same", strides=(1, 1), dilations=(1, 1),
                     accumulator=O.EXACT64, round_mode=O.HALF_AWAY)
         _, acc, kern = gpu_conv(case)
-        assert kern.startswith("lutconv_fast")
+        assert kern != "lutconv_generic"
         s1, z1 = O.compute_coeffs(*case["in_range"], mode)
         s2, z2 = O.compute_coeffs(*case["f_range"], mode)
         xc = torch.from_numpy(O.quantize_values(x, s1, z1, mode).astype(np.float64)).cuda()
