@@ -437,8 +437,8 @@ struct Variant {
 static const Variant kVariants[] = {
     {"auto", 0, 0, 0, 0},
     {"tm4tn16_w8x1", 4, 16, 8, 1},  {"tm4tn16_w4x2", 4, 16, 4, 2},  {"tm4tn16_w2x4", 4, 16, 2, 4},
-    {"tm4tn8_w8x2", 4, 8, 8, 2},    {"tm4tn8_w4x4", 4, 8, 4, 4},    {"tm4tn8_w16x1", 4, 8, 16, 1},
-    {"tm4tn16_w12x1", 4, 16, 12, 1}, {"tm4tn16_w6x2", 4, 16, 6, 2}, {"tm4tn16_w3x4", 4, 16, 3, 4},
+    {"tm4tn8_w8x2", 4, 8, 8, 2},    {"tm4tn8_w4x4", 4, 8, 4, 4},    {"tm2tn16_w12x1", 2, 16, 12, 1},
+    {"tm4tn8_w6x2", 4, 8, 6, 2}, {"tm4tn16_w6x2", 4, 16, 6, 2}, {"tm4tn16_w3x4", 4, 16, 3, 4},
     {"tm2tn16_w16x1", 2, 16, 16, 1}, {"tm2tn16_w8x2", 2, 16, 8, 2}, {"tm4tn16_w4x4", 4, 16, 4, 4},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -476,8 +476,8 @@ static int launch_variant(int v, const ConvK &k, int sm_limit, cudaStream_t s) {
         case 3: return launch_fast<4, 16, 2, 4, SGN>(k, sm_limit, s, nm);
         case 4: return launch_fast<4, 8, 8, 2, SGN>(k, sm_limit, s, nm);
         case 5: return launch_fast<4, 8, 4, 4, SGN>(k, sm_limit, s, nm);
-        case 6: return launch_fast<4, 8, 16, 1, SGN>(k, sm_limit, s, nm);
-        case 7: return launch_fast<4, 16, 12, 1, SGN>(k, sm_limit, s, nm);
+        case 6: return launch_fast<2, 16, 12, 1, SGN>(k, sm_limit, s, nm);
+        case 7: return launch_fast<4, 8, 6, 2, SGN>(k, sm_limit, s, nm);
         case 8: return launch_fast<4, 16, 6, 2, SGN>(k, sm_limit, s, nm);
         case 9: return launch_fast<4, 16, 3, 4, SGN>(k, sm_limit, s, nm);
         case 10: return launch_fast<2, 16, 16, 1, SGN>(k, sm_limit, s, nm);
