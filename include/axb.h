@@ -52,11 +52,17 @@ extern "C" {
 #define AXB_ACC_WRAP32 1
 #define AXB_ACC_SATURATE32 2
 
-/* QuantParams (quantizer.py:60-74); lives in device memory for the kernels */
+/* QuantParams (quantizer.py:60-74) plus the exact code-boundary table of the
+ * quantizer for these parameters: bound[u] = the smallest float32 x whose code
+ * (quantizer.py:120-131) is >= lo + u (u = 1..255; bound[0] = -inf; +inf when
+ * no float reaches that code).  quantize_values is monotone in x, so
+ * code(x) = lo + max{u : bound[u] <= x} exactly; the boundaries are found by
+ * bisection against the fp64 reference function.  Lives in device memory. */
 typedef struct axb_qparams {
     double scale;
     int32_t zero_point;
     int32_t valid; /* 1 once computed */
+    float bound[256];
 } axb_qparams;
 
 typedef struct axb_lut axb_lut; /* opaque: device copies of one truth table */

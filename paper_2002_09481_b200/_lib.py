@@ -36,7 +36,9 @@ c_vp = ctypes.c_void_p
 
 
 class QParams(ctypes.Structure):
-    _fields_ = [("scale", c_dbl), ("zero_point", c_i32), ("valid", c_i32)]
+    _fields_ = [("scale", c_dbl), ("zero_point", c_i32), ("valid", c_i32), ("bound", ctypes.c_float * 256)]
+
+QPARAMS_BYTES = 16 + 4 * 256
 
 
 class ConvDesc(ctypes.Structure):

@@ -38,6 +38,9 @@ __host__ __device__ inline double apply_round(double x, int mode) {
     return trunc(x);                                                            // :56
 }
 
+__host__ __device__ inline int quantize_one(float v, double scale, int zp, int is_signed, int round_mode);
+__host__ __device__ inline void fill_bounds(axb_qparams &p, int is_signed, int round_mode, int u0, int ustep);
+
 __host__ __device__ inline axb_qparams coeffs(double mn, double mx, int is_signed, int round_mode) {
     mn = (0.0 < mn) ? 0.0 : mn;  // Python min(rng.min, 0.0): first arg unless 0.0 < it
     mx = (0.0 > mx) ? 0.0 : mx;  // Python max(rng.max, 0.0): first arg unless 0.0 > it
@@ -55,7 +58,7 @@ __host__ __device__ inline axb_qparams coeffs(double mn, double mx, int is_signe
 }
 
 // ---- quantize_values (quantizer.py:120-131) for one element; returns the code value
-__device__ __forceinline__ int quantize_one(float v, double scale, int zp, int is_signed, int round_mode) {
+__host__ __device__ inline int quantize_one(float v, double scale, int zp, int is_signed, int round_mode) {
     const double x = (double)v / scale;  // IEEE div.rn.f64
     const double nearest = rint(x);
     const double ax = fabs(x);
@@ -73,6 +76,50 @@ __device__ __forceinline__ int quantize_one(float v, double scale, int zp, int i
     double c = r + (double)zp;
     c = c < lo ? lo : (c > hi ? hi : c);
     return (int)c;
+}
+
+// ---- exact code boundaries (see axb_qparams.bound)
+// smallest finite float x (in the total order of floats) with q(x) >= target;
+// -inf if even -FLT_MAX reaches it, +inf if FLT_MAX does not.
+__host__ __device__ inline float code_boundary(int target, double scale, int zp, int is_signed, int round_mode) {
+    const int64_t LO = f2ord(-3.402823466e38f), HI = f2ord(3.402823466e38f);
+    auto q = [&](int64_t o) { return quantize_one(ord2f((int32_t)o), scale, zp, is_signed, round_mode); };
+    if (q(LO) >= target) return -INFINITY;
+    if (q(HI) < target) return INFINITY;
+    // analytic guess ((target - zp) - 0.5) * scale, then an exponential bracket, then bisection
+    double g = ((double)(target - zp) - 0.5) * scale;
+    g = g < -3.4e38 ? -3.4e38 : (g > 3.4e38 ? 3.4e38 : g);
+    int64_t a, b, c0 = f2ord((float)g);
+    if (q(c0) >= target) {  // move down until below target
+        b = c0;
+        int64_t step = 1;
+        a = c0 - 1 < LO ? LO : c0 - 1;
+        while (a > LO && q(a) >= target) {
+            b = a;
+            step *= 2;
+            a = c0 - step < LO ? LO : c0 - step;
+        }
+    } else {
+        a = c0;
+        int64_t step = 1;
+        b = c0 + 1 > HI ? HI : c0 + 1;
+        while (b < HI && q(b) < target) {
+            a = b;
+            step *= 2;
+            b = c0 + step > HI ? HI : c0 + step;
+        }
+    }
+    while (b - a > 1) {  // invariant q(a) < target <= q(b)
+        const int64_t m = a + (b - a) / 2;
+        if (q(m) >= target) b = m; else a = m;
+    }
+    return ord2f((int32_t)b);
+}
+
+__host__ __device__ inline void fill_bounds(axb_qparams &p, int is_signed, int round_mode, int u0, int ustep) {
+    const int lo = is_signed ? -128 : 0;
+    for (int u = u0; u < 256; u += ustep)
+        p.bound[u] = u == 0 ? -INFINITY : code_boundary(lo + u, p.scale, p.zero_point, is_signed, round_mode);
 }
 
 // ---- warp reductions

@@ -28,7 +28,6 @@ namespace axb {
 
 constexpr int kMaxTaps = 256;
 constexpr int kStages = 4;
-constexpr int kThreads = 256;
 
 struct ConvK {
     const uint8_t *codes;
@@ -171,7 +170,9 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     uint8_t *w_s = act_s + kStages * ACT_STAGE;
     int32_t *tapoff_s = reinterpret_cast<int32_t *>(w_s + kStages * W_STAGE);
     int32_t *tappix_s = tapoff_s + kMaxTaps;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(tappix_s + kMaxTaps);
+    int64_t *ep_cc = reinterpret_cast<int64_t *>(tappix_s + kMaxTaps);  // BN per-channel constants
+    float *ep_bias = reinterpret_cast<float *>(ep_cc + BN);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(ep_bias + BN + (BN & 1));
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -331,12 +332,20 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         const int64_t m0 = (c_tile / p.ntn) * BM;
         const int n0 = (int)(c_tile % p.ntn) * BN;
         c_tile += gridDim.x;
+        // per-channel constants of this tile: K*zp1*zp2 - zp1*S_f[c] (int64) and the bias
+        if (tid < BN) {
+            const int c = n0 + tid;
+            ep_cc[tid] = c < p.cout ? e.kzz - e.zp1 * p.fsum[c] : 0;
+            ep_bias[tid] = (p.bias && c < p.cout) ? p.bias[c] : 0.0f;
+        }
+        __syncthreads();
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
             const int64_t m = m0 + wm * 32 * TM + i * 32 + lane;
             if (m < p.M) {
                 const int64_t sp = patch_sum(p, m, tappix_s);
                 psum_ovf |= (sp > INT32_MAX || sp < INT32_MIN);
+                const int64_t pz = -e.zp2 * sp;
                 float y[TN];
 #pragma unroll
                 for (int j = 0; j < TN; ++j) {
@@ -352,8 +361,14 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
                                 A = A > INT32_MAX ? INT32_MAX : (A < INT32_MIN ? INT32_MIN : A);
                         }
                         if (p.acc_out) p.acc_out[m * p.cout + c] = A;
-                        y[j] = finish(p, e, A, sp, m, c);
-                        track(y[j], tmin, tmax, nonfinite);
+                        // corr = A - zp2*Sp - zp1*Sf + K*zp1*zp2 (axconv.py:249-254)
+                        const int64_t corr = A + pz + ep_cc[wn * TN + j];
+                        float v = __double2float_rn(e.scale * __ll2double_rn(corr));  // axconv.py:256
+                        if (p.bias) v = __fadd_rn(v, ep_bias[wn * TN + j]);           // graph.py:268-269
+                        if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + c]);  // graph.py:282-286
+                        if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;             // np.maximum(x, 0)
+                        y[j] = v;
+                        track(v, tmin, tmax, nonfinite);
                     }
                 }
                 const int cb = n0 + wn * TN;
@@ -446,7 +461,7 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 template <int TM, int TN, int WM, int WN, bool SGN>
 static int launch_fast(const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WM * 32 * TM, BN = WN * TN;
-    const size_t smem = kLutBytes + kStages * (BM * 16 + 16 * BN * 2) + 2 * kMaxTaps * 4 + 16;
+    const size_t smem = kLutBytes + kStages * (BM * 16 + 16 * BN * 2) + 2 * kMaxTaps * 4 + BN * 12 + 8 + 16;
     auto fn = lutconv_fast<TM, TN, WM, WN, SGN>;
     static int configured_dev = -1;  // one per instantiation
     int dev = 0;
@@ -487,10 +502,20 @@ static int launch_variant(int v, const ConvK &k, int sm_limit, cudaStream_t s) {
     }
 }
 
+// Heuristic from scripts/tune_variants.py on B200 (ResNet-8 / ResNet-50 layers):
+// 16-warp TN=8 tiles win for narrow layers, the 12-warp 384x64 tile for wide
+// ones unless its tile count quantizes badly against the SM count.
 static int pick_variant(const ConvK &k) {
-    if (k.coutp <= 16) return 1;
-    if (k.coutp <= 32) return 2;
-    return 3;
+    if (k.coutp <= 16) return 4;   // tm4tn8_w8x2: 1024 x 16
+    if (k.coutp <= 32) return 5;   // tm4tn8_w4x4:  512 x 32
+    const int64_t sms = sm_count();
+    auto eff = [&](int64_t bm, int64_t bn) {
+        const int64_t tiles = ((k.M + bm - 1) / bm) * ((k.coutp + bn - 1) / bn);
+        const int64_t waves = (tiles + sms - 1) / sms;
+        return (double)tiles / (double)(waves * sms);
+    };
+    const double e9 = eff(384, 64), e5 = eff(512, 32);
+    return (e5 > e9 + 0.08) ? 5 : 9;  // tm4tn16_w3x4: 384 x 64
 }
 
 }  // namespace axb

@@ -50,130 +50,142 @@ __global__ void range_reset_kernel(int32_t *d_range) {
     d_range[1] = INT32_MIN;
 }
 
-__global__ void coeffs_kernel(const int32_t *d_range, int is_signed, int round_mode, axb_qparams *out) {
-    // an empty/unwritten range (min > max) never reaches here: the host checks flags
+// coefficients of a device range + the exact code-boundary table: 256 threads,
+// thread u bisects boundary u against the fp64 quantizer (no host sync)
+__global__ void __launch_bounds__(256) coeffs_kernel(const int32_t *d_range, int is_signed, int round_mode,
+                                                     axb_qparams *out) {
     const float mn = ord2f(d_range[0]);
     const float mx = ord2f(d_range[1]);
-    *out = coeffs((double)mn, (double)mx, is_signed, round_mode);
+    axb_qparams p = coeffs((double)mn, (double)mx, is_signed, round_mode);
+    const int u = threadIdx.x;
+    const int lo = is_signed ? -128 : 0;
+    out->bound[u] = u == 0 ? -INFINITY : code_boundary(lo + u, p.scale, p.zero_point, is_signed, round_mode);
+    if (u == 0) {
+        out->scale = p.scale;
+        out->zero_point = p.zero_point;
+        out->valid = 1;
+    }
 }
 
-__global__ void params_set_kernel(axb_qparams p, axb_qparams *out) { *out = p; }
+__global__ void params_set_kernel(axb_qparams p, axb_qparams *out) {
+    for (int u = threadIdx.x; u < 256; u += blockDim.x) out->bound[u] = p.bound[u];
+    if (threadIdx.x == 0) {
+        out->scale = p.scale;
+        out->zero_point = p.zero_point;
+        out->valid = p.valid;
+    }
+}
 
 // ---------------------------------------------------------------- K2: quantize + pad
-// Small-channel mode (cs <= 16): one thread per padded pixel, writes cs bytes.
-template <int CS>
-__global__ void __launch_bounds__(256) quantize_pad_small(const float *__restrict__ x, int64_t n, int64_t h,
-                                                          int64_t w, int c, int pt, int pl, int64_t hp,
-                                                          int64_t wp, const axb_qparams *__restrict__ prm,
-                                                          int is_signed, int round_mode,
-                                                          uint8_t *__restrict__ codes, int32_t *__restrict__ pixsum,
-                                                          int32_t *d_flags) {
-    const double scale = prm->scale;
-    const int zp = prm->zero_point;
-    const int64_t total = n * hp * wp;
-    int nonfinite = 0;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t xw = p % wp;
-        const int64_t t = p / wp;
-        const int64_t yh = t % hp;
-        const int64_t b = t / hp;
-        const int64_t iy = yh - pt, ix = xw - pl;
-        uint8_t outb[CS];
-        int32_t s = 0;
-        if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
-            const float *src = x + ((b * h + iy) * w + ix) * c;
-#pragma unroll
-            for (int ci = 0; ci < CS; ++ci) {
-                if (ci < c) {
-                    const float v = src[ci];
-                    nonfinite |= !isfinite(v);
-                    const int q = quantize_one(v, scale, zp, is_signed, round_mode);
-                    s += q;
-                    outb[ci] = (uint8_t)(q & 0xFF);
-                } else {
-                    outb[ci] = 0;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int ci = 0; ci < CS; ++ci) outb[ci] = ci < c ? (uint8_t)(zp & 0xFF) : (uint8_t)0;
-            s = zp * c;
-        }
-        uint8_t *dst = codes + p * CS;
-        if (CS == 4) {
-            *reinterpret_cast<uint32_t *>(dst) =
-                outb[0] | (outb[1 % CS] << 8) | (outb[2 % CS] << 16) | ((uint32_t)outb[3 % CS] << 24);
-        } else {
-#pragma unroll
-            for (int q = 0; q < CS / 4; ++q)
-                reinterpret_cast<uint32_t *>(dst)[q] = outb[4 * q] | (outb[4 * q + 1] << 8) |
-                                                       (outb[4 * q + 2] << 16) | ((uint32_t)outb[4 * q + 3] << 24);
-        }
-        pixsum[p] = s;
+// Exact quantization without per-element fp64: an fp32 estimate of the code
+// offset, corrected against the exact boundary table (qparams.bound, staged in
+// shared memory) -- usually 2 compares.  One thread per 4-channel group
+// (float4 in, u32 out, fully coalesced); the per-pixel code sum is a segmented
+// warp reduction over the G = cs/4 groups of a pixel (G a power of two <= 32),
+// or a warp per pixel (G == 0: cs > 128 or not a power of two).
+struct QuantCtx {
+    float bnd[257];
+    float inv, zpo;
+    int lo, zp;
+};
+
+__device__ __forceinline__ void quant_ctx_load(QuantCtx &q, const axb_qparams *prm, int is_signed) {
+    for (int u = threadIdx.x; u < 256; u += blockDim.x) q.bnd[u] = prm->bound[u];
+    if (threadIdx.x == 0) {
+        q.bnd[256] = INFINITY;
+        q.lo = is_signed ? -128 : 0;
+        q.zp = prm->zero_point;
+        q.inv = (float)(1.0 / prm->scale);
+        q.zpo = (float)(prm->zero_point - q.lo);
     }
-    range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
+    __syncthreads();
 }
 
-// Wide mode (cs % 16 == 0, cs >= 32): one warp per padded pixel; lane handles
-// 4 channels per step (float4 read, u32 write), warp-reduces the code sum.
-__global__ void __launch_bounds__(256) quantize_pad_wide(const float *__restrict__ x, int64_t n, int64_t h,
-                                                         int64_t w, int c, int64_t cs, int pt, int pl, int64_t hp,
-                                                         int64_t wp, const axb_qparams *__restrict__ prm,
-                                                         int is_signed, int round_mode, uint8_t *__restrict__ codes,
-                                                         int32_t *__restrict__ pixsum, int32_t *d_flags) {
-    const double scale = prm->scale;
-    const int zp = prm->zero_point;
+// code value of a finite float: lo + max{u : bnd[u] <= x}
+__device__ __forceinline__ int quant_exact(const QuantCtx &q, float x) {
+    float uf = fmaf(x, q.inv, q.zpo);
+    int u = (uf > 0.0f) ? (uf < 255.0f ? __float2int_rn(uf) : 255) : 0;  // NaN / -inf -> 0
+    while (x < q.bnd[u]) --u;        // bnd[0] = -inf stops it
+    while (x >= q.bnd[u + 1]) ++u;   // bnd[256] = +inf stops it
+    return q.lo + u;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restrict__ x, int64_t n, int64_t h, int64_t w,
+                                                           int c, int64_t cs, int pt, int pl, int64_t hp, int64_t wp,
+                                                           const axb_qparams *__restrict__ prm, int is_signed,
+                                                           uint8_t *__restrict__ codes, int32_t *__restrict__ pixsum,
+                                                           int32_t *d_flags) {
+    __shared__ QuantCtx q;
+    quant_ctx_load(q, prm, is_signed);
     const int lane = threadIdx.x & 31;
-    const int64_t total = n * hp * wp;
-    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t npix = n * hp * wp;
     const bool vec = (c % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    const int zpb = q.zp & 0xFF;
     int nonfinite = 0;
-    for (int64_t p = warp0; p < total; p += nwarps) {
+    auto group = [&](int64_t p, int64_t g, int32_t &s) -> uint32_t {
         const int64_t xw = p % wp;
         const int64_t t = p / wp;
         const int64_t yh = t % hp;
         const int64_t b = t / hp;
         const int64_t iy = yh - pt, ix = xw - pl;
-        const bool inside = iy >= 0 && iy < h && ix >= 0 && ix < w;
-        const float *src = x + ((b * h + (inside ? iy : 0)) * w + (inside ? ix : 0)) * c;
-        uint32_t *dst = reinterpret_cast<uint32_t *>(codes + p * cs);
-        int32_t s = 0;
-        for (int64_t g = lane; g < cs / 4; g += 32) {
-            const int64_t c0 = g * 4;
-            uint32_t word = 0;
-            if (inside) {
-                float e[4];
-                if (vec && c0 + 3 < c) {
-                    const float4 v = __ldg(reinterpret_cast<const float4 *>(src + c0));
-                    e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) e[q] = (c0 + q < c) ? src[c0 + q] : 0.0f;
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (c0 + q < c) {
-                        nonfinite |= !isfinite(e[q]);
-                        const int qv = quantize_one(e[q], scale, zp, is_signed, round_mode);
-                        s += qv;
-                        word |= (uint32_t)(qv & 0xFF) << (8 * q);
-                    }
-                }
+        const int c0 = (int)g * 4;
+        uint32_t word = 0;
+        if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
+            const float *src = x + ((b * h + iy) * w + ix) * c + c0;
+            float e[4];
+            if (vec && c0 + 3 < c) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
+                e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
             } else {
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (c0 + q < c) {
-                        s += zp;
-                        word |= (uint32_t)(zp & 0xFF) << (8 * q);
-                    }
+                for (int k = 0; k < 4; ++k) e[k] = (c0 + k < c) ? src[k] : 0.0f;
             }
-            dst[g] = word;
-        }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) pixsum[p] = s;
+            for (int k = 0; k < 4; ++k) {
+                if (c0 + k < c) {
+                    nonfinite |= !isfinite(e[k]);
+                    const int code = quant_exact(q, e[k]);
+                    s += code;
+                    word |= (uint32_t)(code & 0xFF) << (8 * k);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (c0 + k < c) {
+                    s += q.zp;
+                    word |= (uint32_t)zpb << (8 * k);
+                }
+        }
+        return word;
+    };
+    if constexpr (G > 0) {
+        const int64_t total = npix * G;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        const int64_t bound = (total + 31) / 32 * 32;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < bound; i += stride) {
+            int32_t s = 0;
+            if (i < total) {
+                const int64_t p = i / G;
+                const uint32_t word = group(p, i % G, s);
+                reinterpret_cast<uint32_t *>(codes)[i] = word;  // cs == 4G: group i is word i
+            }
+#pragma unroll
+            for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (i < total && (i % G) == 0) pixsum[i / G] = s;
+        }
+    } else {
+        const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+        const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        for (int64_t p = warp0; p < npix; p += nwarps) {
+            int32_t s = 0;
+            for (int64_t g = lane; g < cs / 4; g += 32)
+                reinterpret_cast<uint32_t *>(codes + p * cs)[g] = group(p, g, s);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) pixsum[p] = s;
+        }
     }
     range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
 }
@@ -338,17 +350,18 @@ int axb_coeffs_host(double mn, double mx, int is_signed, int round_mode, axb_qpa
         return set_error(AXB_E_VALUE, "range must be finite");
     if (mn > mx) return set_error(AXB_E_VALUE, "range min exceeds max");
     *out = coeffs(mn, mx, is_signed, round_mode);
+    fill_bounds(*out, is_signed, round_mode, 0, 1);
     return AXB_OK;
 }
 
 int axb_coeffs_from_range(const int32_t *d_range, int is_signed, int round_mode, axb_qparams *d_out,
                           void *stream) {
-    coeffs_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_range, is_signed, round_mode, d_out);
+    coeffs_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_range, is_signed, round_mode, d_out);
     return check_launch("coeffs_from_range");
 }
 
 int axb_params_upload(const axb_qparams *host_params, axb_qparams *d_params, void *stream) {
-    params_set_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(*host_params, d_params);
+    params_set_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(*host_params, d_params);
     return check_launch("params_upload");
 }
 
@@ -361,17 +374,22 @@ int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t 
     if (total == 0) return AXB_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cap = (int64_t)sm_count() * 16;
-    if (cs <= 16) {
-        int64_t blocks = (total + 255) / 256;
-        if (blocks > cap) blocks = cap;
-        quantize_pad_small<16><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, pt, pl, hp, wp, d_params,
-                                                           is_signed, round_mode, d_codes, d_pixsum, d_flags);
-    } else {
-        int64_t blocks = (total * 32 + 255) / 256;
-        if (blocks > cap) blocks = cap;
-        quantize_pad_wide<<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, cs, pt, pl, hp, wp, d_params, is_signed,
-                                                      round_mode, d_codes, d_pixsum, d_flags);
+    const int64_t G = cs / 4;
+    const int64_t work = (G <= 32 && (G & (G - 1)) == 0) ? total * G : total * 32;
+    int64_t blocks = (work + 255) / 256;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+#define AXB_QLAUNCH(GG)                                                                                             \
+    quantize_pad_kernel<GG><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, cs, pt, pl, hp, wp, d_params, is_signed, \
+                                                        d_codes, d_pixsum, d_flags)
+    switch (G) {
+        case 4: AXB_QLAUNCH(4); break;
+        case 8: AXB_QLAUNCH(8); break;
+        case 16: AXB_QLAUNCH(16); break;
+        case 32: AXB_QLAUNCH(32); break;
+        default: AXB_QLAUNCH(0); break;
     }
+#undef AXB_QLAUNCH
     return check_launch("quantize_pad");
 }
 

@@ -48,7 +48,7 @@ class ConvLayer:
         self.kpad = int(lib.axb_filter_kpad(fk[0], fk[1], fk[3]))
         self.coutp = int(lib.axb_filter_coutp(self.cout))
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        self.params = torch.zeros(2, 16, dtype=torch.uint8, device=self.device)  # [input, filter] axb_qparams
+        self.params = torch.zeros(2, _lib.QPARAMS_BYTES, dtype=torch.uint8, device=self.device)  # [input, filter] axb_qparams
         hp = _lib.QParams()
         _lib.check(lib.axb_coeffs_host(float(f_range[0]), float(f_range[1]), self.sgn, self.round, hp))
         _lib.check(lib.axb_params_upload(hp, self.params[1].data_ptr(), stream))

@@ -138,3 +138,45 @@ def test_missing_library_raises(tmp_path):
 
     with pytest.raises(_lib.AxbError, match="no CPU fallback"):
         _lib.load(tmp_path / "nope.so")
+
+
+def _codes_from_bounds(p, vals, signed):
+    b = np.array(p.bound, np.float32)
+    lo = -128 if signed else 0
+    # lo + max{u : bound[u] <= x}
+    return (lo + np.searchsorted(b, vals.astype(np.float32), side="right") - 1).astype(np.int64)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_exact_code_boundary_tables(seed):
+    """The boundary table reproduces the reference quantizer bit-for-bit (host build of the device code)."""
+    from paper_2002_09481_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(seed)
+    rounds = [O.HALF_AWAY, O.HALF_EVEN, O.TOWARD_ZERO]
+    ranges = [(-2.3, 5.9), (0.0, 1.0), (0.0, 0.0), (-1e6, 1e6), (0.0, 1e-9), (-9.0, -1.0), (-1e-3, 1e5),
+              (0.0, 5e-324), (-3e38, 3e38), (1e-40, 1e-39)]
+    for _ in range(6):
+        lo = float(rng.uniform(-50, 5)) * 10.0 ** int(rng.integers(-8, 4))
+        ranges.append((lo, lo + abs(float(rng.standard_normal())) * 10.0 ** int(rng.integers(-8, 4))))
+    for mn, mx in ranges:
+        for sgn in (0, 1):
+            for rm in range(3):
+                p = _lib.QParams()
+                _lib.check(lib.axb_coeffs_host(mn, mx, sgn, rm, p))
+                mode = O.SIGNED if sgn else O.UNSIGNED
+                span = max(abs(mn), abs(mx), 1e-30)
+                vals = np.concatenate([
+                    rng.uniform(-1.2 * span, 1.2 * span, 3000),
+                    (np.arange(-300, 300) + 0.5) * p.scale, (np.arange(-300, 300)) * p.scale,
+                    np.nextafter(np.float32((np.arange(-300, 300) + 0.5) * p.scale), np.float32(np.inf)),
+                    np.nextafter(np.float32((np.arange(-300, 300) + 0.5) * p.scale), np.float32(-np.inf)),
+                    np.array([0.0, -0.0, 1e-45, -1e-45, 3.4e38, -3.4e38]),
+                ]).astype(np.float32)
+                vals = vals[np.isfinite(vals)]
+                b = np.array(p.bound, np.float32)
+                assert b[0] == -np.inf and np.all(np.diff(b) >= 0)
+                want = O.quantize_values(vals, p.scale, p.zero_point, mode, rounds[rm]).astype(np.int64)
+                got = _codes_from_bounds(p, vals, sgn)
+                assert np.array_equal(got, want), (mn, mx, sgn, rm)

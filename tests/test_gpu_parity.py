@@ -191,16 +191,16 @@ def test_quantize_kernel_codes_match_reference():
         hp_ = _lib.QParams()
         _lib.check(lib.axb_coeffs_host(float(mn), float(mx), sgn, rm, hp_))
         assert (hp_.scale, hp_.zero_point) == (g[f"q{i}_coeffs"][0], int(g[f"q{i}_coeffs"][1]))
-        prm = torch.zeros(16, dtype=torch.uint8, device="cuda")
+        prm = torch.zeros(_lib.QPARAMS_BYTES, dtype=torch.uint8, device="cuda")
         _lib.check(lib.axb_params_upload(hp_, prm.data_ptr(), s))
         x = torch.from_numpy(vals.reshape(1, 1, -1, 1)).cuda()
         n = vals.size
-        codes = torch.empty(n * 4 + 8, dtype=torch.uint8, device="cuda")  # cs = 4, 1 pad col each side
+        codes = torch.empty((n + 2) * 16, dtype=torch.uint8, device="cuda")  # cs = 16, 1 pad col each side
         pixsum = torch.empty(n + 2, dtype=torch.int32, device="cuda")
         fl = torch.zeros(1, dtype=torch.int32, device="cuda")
-        _lib.check(lib.axb_quantize_pad(x.data_ptr(), 1, 1, n, 1, 0, 0, 1, 1, 4, prm.data_ptr(), sgn, rm,
+        _lib.check(lib.axb_quantize_pad(x.data_ptr(), 1, 1, n, 1, 0, 0, 1, 1, 16, prm.data_ptr(), sgn, rm,
                                         codes.data_ptr(), pixsum.data_ptr(), fl.data_ptr(), s))
-        cb = codes.cpu().numpy().reshape(n + 2, 4)
+        cb = codes.cpu().numpy().reshape(n + 2, 16)
         want = g[f"q{i}_codes"]
         assert np.array_equal(cb[1:-1, 0].view(np.int8 if sgn else np.uint8), want), i
         assert (cb[[0, -1], 0] == (hp_.zero_point & 0xFF)).all()
