@@ -135,6 +135,7 @@ typedef struct axb_conv_desc {
     int32_t force_generic;  /* 1: use the int64 generic kernel (testing)            */
     int32_t sm_limit;       /* 0 = all SMs; else cap persistent grid                 */
     int32_t variant;        /* fast-kernel tile variant, 0 = heuristic (tuning)      */
+    int32_t pixel_order;    /* lanes -> pixels: 0 auto, 1 row runs, 4 4x8 blocks     */
 } axb_conv_desc;
 
 int axb_conv2d_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);

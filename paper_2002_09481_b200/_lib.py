@@ -55,7 +55,7 @@ class ConvDesc(ctypes.Structure):
         ("accumulator", c_i32), ("relu", c_i32),
         ("bias", c_vp), ("residual", c_vp), ("out", c_vp), ("acc_out", c_vp),
         ("out_range", c_vp), ("flags", c_vp),
-        ("force_generic", c_i32), ("sm_limit", c_i32), ("variant", c_i32),
+        ("force_generic", c_i32), ("sm_limit", c_i32), ("variant", c_i32), ("pixel_order", c_i32),
     ]
 
 

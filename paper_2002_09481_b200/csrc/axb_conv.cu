@@ -52,6 +52,7 @@ struct ConvK {
     int32_t f00;          // lut[0] as a value (junk-tap contribution)
     int32_t ntn;
     int64_t ntiles;
+    int32_t blk;  // 1: lanes = 32 consecutive pixels of a row; 4: lanes = a 4x8 pixel block
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -117,6 +118,29 @@ __device__ __forceinline__ EpiConst epi_const(const ConvK &p) {
     return e;
 }
 
+// Tile-order position -> NHWC output pixel index m, and the padded-input pixel
+// index of its window origin.  blk == 4 walks each image in 4-row bands of
+// 4x8 blocks so a warp instruction's 32 lanes are a compact pixel block (more
+// similar codes -> fewer LUT bank conflicts); needs oh % 4 == 0, ow % 8 == 0.
+__device__ __forceinline__ int64_t pixel_of(const ConvK &p, int64_t mt, int64_t &pix0) {
+    const int64_t hw = (int64_t)p.oh * p.ow;
+    const int64_t b = mt / hw;
+    const int64_t r = mt - b * hw;
+    int64_t oy, ox;
+    if (p.blk == 4) {
+        const int64_t band = r / (4 * p.ow);
+        const int64_t rr = r - band * 4 * p.ow;
+        const int64_t bx = rr >> 5, s = rr & 31;
+        oy = band * 4 + (s >> 3);
+        ox = bx * 8 + (s & 7);
+    } else {
+        oy = r / p.ow;
+        ox = r - oy * p.ow;
+    }
+    pix0 = (b * p.hp + oy * p.sh) * (int64_t)p.wp + ox * p.sw;
+    return b * hw + oy * p.ow + ox;
+}
+
 // patch sum S_p of output pixel m (axconv.py:193), int64, from per-pixel code sums
 __device__ __forceinline__ int64_t patch_sum(const ConvK &p, int64_t m, const int32_t *tappix) {
     const int64_t ox = m % p.ow;
@@ -144,6 +168,12 @@ __device__ __forceinline__ void track(float y, int32_t &tmin, int32_t &tmax, int
     const int32_t o = f2ord(y);
     tmin = min(tmin, o);
     tmax = max(tmax, o);
+}
+// float min/max tracker for the fast epilogue (+-0 order is irrelevant to compute_coeffs)
+__device__ __forceinline__ void track(float y, float &fmin, float &fmax, int &nonfinite) {
+    nonfinite |= !(fabsf(y) <= 3.402823466e38f);
+    fmin = fminf(fmin, y);
+    fmax = fmaxf(fmax, y);
 }
 
 // ---------------------------------------------------------------- fast kernel
@@ -196,7 +226,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     }
 
     const EpiConst e = epi_const(p);
-    int32_t tmin = INT32_MAX, tmax = INT32_MIN;
+    float tmin = INFINITY, tmax = -INFINITY;
     int nonfinite = 0, psum_ovf = 0;
     const uint32_t lut_base = smem_u32(smem);
 
@@ -214,13 +244,11 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         ld_n0 = (int)(tile % p.ntn) * BN;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            const int64_t m = m0 + tid + q * NT;
-            if (m < p.M) {
-                const int64_t ox = m % p.ow;
-                const int64_t t = m / p.ow;
-                const int64_t oy = t % p.oh;
-                const int64_t b = t / p.oh;
-                rowbase[q] = (int32_t)(((b * p.hp + oy * p.sh) * p.wp + ox * p.sw) * p.cs);
+            const int64_t mt = m0 + tid + q * NT;
+            if (mt < p.M) {
+                int64_t pix0;
+                pixel_of(p, mt, pix0);
+                rowbase[q] = (int32_t)(pix0 * p.cs);
             } else {
                 rowbase[q] = -1;
             }
@@ -328,59 +356,81 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
 
         if (++c_kc < p.nchunks) continue;
         // ------------------------------------------------ fused epilogue for tile c_tile
+        // In this kernel kpad <= 32768, so |A| < 2^31: WRAP32 and SATURATE32 are the
+        // identity on the exact sum (axconv.py:128-133) and A = acc - junk exactly.
         c_kc = 0;
         const int64_t m0 = (c_tile / p.ntn) * BM;
         const int n0 = (int)(c_tile % p.ntn) * BN;
         c_tile += gridDim.x;
-        // per-channel constants of this tile: K*zp1*zp2 - zp1*S_f[c] (int64) and the bias
-        if (tid < BN) {
+        if (tid < BN) {  // per-channel constants: K*zp1*zp2 - zp1*S_f[c] - junk, bias
             const int c = n0 + tid;
-            ep_cc[tid] = c < p.cout ? e.kzz - e.zp1 * p.fsum[c] : 0;
+            ep_cc[tid] = c < p.cout ? e.kzz - e.zp1 * p.fsum[c] - e.junk : 0;
             ep_bias[tid] = (p.bias && c < p.cout) ? p.bias[c] : 0.0f;
         }
         __syncthreads();
+        const int cb = n0 + wn * TN;
+        const bool full = cb + TN <= p.cout && (p.cout & 3) == 0;
+        const int64_t *cc = ep_cc + wn * TN;
+        const float *bs = ep_bias + wn * TN;
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
-            const int64_t m = m0 + wm * 32 * TM + i * 32 + lane;
-            if (m < p.M) {
-                const int64_t sp = patch_sum(p, m, tappix_s);
+            const int64_t mt = m0 + wm * 32 * TM + i * 32 + lane;  // position in tile order
+            if (mt < p.M) {
+                int64_t pix0;
+                const int64_t m = pixel_of(p, mt, pix0);  // NHWC output pixel + its window origin
+                int64_t sp = 0;                            // S_p (axconv.py:193)
+                for (int t = 0; t < p.taps; ++t) sp += p.pixsum[pix0 + tappix_s[t]];
                 psum_ovf |= (sp > INT32_MAX || sp < INT32_MIN);
                 const int64_t pz = -e.zp2 * sp;
                 float y[TN];
 #pragma unroll
                 for (int j = 0; j < TN; ++j) {
-                    const int c = n0 + wn * TN + j;
-                    y[j] = 0.0f;
-                    if (c < p.cout) {
-                        int64_t A;
-                        if (p.acc_mode == AXB_ACC_WRAP32) {
-                            A = (int64_t)(int32_t)((uint32_t)acc[i][j] - (uint32_t)e.junk);
-                        } else {
-                            A = (int64_t)acc[i][j] - e.junk;
-                            if (p.acc_mode == AXB_ACC_SATURATE32)
-                                A = A > INT32_MAX ? INT32_MAX : (A < INT32_MIN ? INT32_MIN : A);
-                        }
-                        if (p.acc_out) p.acc_out[m * p.cout + c] = A;
-                        // corr = A - zp2*Sp - zp1*Sf + K*zp1*zp2 (axconv.py:249-254)
-                        const int64_t corr = A + pz + ep_cc[wn * TN + j];
-                        float v = __double2float_rn(e.scale * __ll2double_rn(corr));  // axconv.py:256
-                        if (p.bias) v = __fadd_rn(v, ep_bias[wn * TN + j]);           // graph.py:268-269
-                        if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + c]);  // graph.py:282-286
-                        if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;             // np.maximum(x, 0)
-                        y[j] = v;
-                        track(v, tmin, tmax, nonfinite);
-                    }
+                    // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254); fp64 dequant (:256)
+                    const int64_t corr = (int64_t)acc[i][j] + pz + cc[j];
+                    y[j] = __double2float_rn(e.scale * __ll2double_rn(corr));
                 }
-                const int cb = n0 + wn * TN;
                 float *dst = p.out + m * p.cout + cb;
-                if (cb + TN <= p.cout && (p.cout & 3) == 0) {
+                if (full) {
+                    if (p.bias) {
+#pragma unroll
+                        for (int j = 0; j < TN; ++j) y[j] = __fadd_rn(y[j], bs[j]);  // graph.py:268-269
+                    }
+                    if (p.residual) {  // graph.py:282-286
+                        const float4 *r4 = reinterpret_cast<const float4 *>(p.residual + m * p.cout + cb);
+#pragma unroll
+                        for (int j = 0; j < TN; j += 4) {
+                            const float4 r = __ldg(r4 + j / 4);
+                            y[j] = __fadd_rn(y[j], r.x); y[j + 1] = __fadd_rn(y[j + 1], r.y);
+                            y[j + 2] = __fadd_rn(y[j + 2], r.z); y[j + 3] = __fadd_rn(y[j + 3], r.w);
+                        }
+                    }
+                    if (p.relu) {
+#pragma unroll
+                        for (int j = 0; j < TN; ++j) y[j] = (y[j] > 0.0f || y[j] != y[j]) ? y[j] : 0.0f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) track(y[j], tmin, tmax, nonfinite);
 #pragma unroll
                     for (int j = 0; j < TN; j += 4)
                         *reinterpret_cast<float4 *>(dst + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
+                    if (p.acc_out) {
+#pragma unroll
+                        for (int j = 0; j < TN; ++j)
+                            p.acc_out[m * p.cout + cb + j] = (int64_t)acc[i][j] - e.junk;
+                    }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < TN; ++j)
-                        if (cb + j < p.cout) dst[j] = y[j];
+                    for (int j = 0; j < TN; ++j) {
+                        if (cb + j < p.cout) {
+                            float v = y[j];
+                            if (p.bias) v = __fadd_rn(v, bs[j]);
+                            if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + cb + j]);
+                            if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;
+                            track(v, tmin, tmax, nonfinite);
+                            dst[j] = v;
+                            if (p.acc_out) p.acc_out[m * p.cout + cb + j] = (int64_t)acc[i][j] - e.junk;
+                        }
+                    }
                 }
             }
 #pragma unroll
@@ -388,7 +438,9 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         }
     }
     cp_async_wait<0>();
-    range_commit(tmin, tmax, nonfinite, p.out_range, p.flags, AXB_FLAG_OUT_NONFINITE);
+    const bool any = tmin <= tmax;
+    range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
+                 AXB_FLAG_OUT_NONFINITE);
     if (psum_ovf) atomicOr(p.flags, AXB_FLAG_PSUM_OVF);
 }
 
@@ -573,6 +625,10 @@ int axb_conv2d_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
         const int64_t per_img = d->hp * d->wp * d->cs;
         int64_t step = ((int64_t(1) << 31) - 1) / (per_img > 0 ? per_img : 1);
         if (step < 1) return set_error(AXB_E_VALUE, "one image's code tensor exceeds 2 GiB");
+        int order = d->pixel_order;
+        if (order == 0) order = (d->oh % 4 == 0 && d->ow % 8 == 0) ? 4 : 1;
+        if (order == 4 && (d->oh % 4 || d->ow % 8)) return set_error(AXB_E_VALUE, "4x8 pixel order needs oh%4==0, ow%8==0");
+        k.blk = order == 4 ? 4 : 1;
         for (int64_t b0 = 0; b0 < d->n; b0 += step) {
             const int64_t nb = (d->n - b0 < step) ? d->n - b0 : step;
             ConvK kc = k;

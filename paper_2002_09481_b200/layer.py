@@ -76,7 +76,7 @@ class ConvLayer:
 
     def run(self, x: torch.Tensor, in_range_dev=None, *, relu=False, residual=None, out_range=None,
             out_flag=None, quant_flag=None, acc_out=None, force_generic=False, sm_limit=0, variant=0,
-            profile=None) -> torch.Tensor:
+            pixel_order=0, profile=None) -> torch.Tensor:
         """x: (n,h,w,cin) fp32 CUDA.  in_range_dev: device int32[2] ordered-float range, or None if
         set_input_params() was called.  Returns (n,oh,ow,cout) fp32."""
         lib = self.lib
@@ -139,6 +139,7 @@ class ConvLayer:
         d.force_generic = int(force_generic)
         d.sm_limit = int(sm_limit)
         d.variant = int(variant)
+        d.pixel_order = int(pixel_order)
         if profile is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--variants", default="")
+    ap.add_argument("--orders", default="", help="compare pixel orders (e.g. 1,4) at the heuristic variant")
     args = ap.parse_args()
     spec = workload_spec(args.workload, "trunc2")
     batch = args.batch or spec["batch"]
@@ -72,6 +73,20 @@ def main():
             elif not torch.equal(ref.view(torch.int32), y.view(torch.int32)):
                 raise SystemExit(f"variant {names[v]} differs on {n['id']}")
             res[names[v]] = round(t, 4)
+        if args.orders:
+            for o in [int(v) for v in args.orders.split(",")]:
+                if o == 4 and (y.shape[1] % 4 or y.shape[2] % 8):
+                    continue
+                times = []
+                for _ in range(6):
+                    prof = []
+                    y2 = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(), variant=0,
+                                   pixel_order=o, profile=prof)
+                    torch.cuda.synchronize()
+                    times.append(prof[0][0].elapsed_time(prof[0][1]))
+                if not torch.equal(ref.view(torch.int32), y2.view(torch.int32)):
+                    raise SystemExit(f"pixel order {o} differs on {n['id']}")
+                res[f"auto_order{o}"] = round(statistics.median(times[1:]), 4)
         best = min(res, key=res.get)
         sm = torch.cuda.get_device_properties(0).multi_processor_count
         peak = sm * 32 * 1.965e9

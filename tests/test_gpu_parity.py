@@ -62,7 +62,7 @@ def test_c1_cases_bit_exact(generic):
         kernels.add(kern.split("<")[0])
         assert bits_equal(y, g[f"out_{i}"]), (i, kern)
         assert np.array_equal(acc, g[f"acc_{i}"]), (i, kern)
-    assert kernels == ({"lutconv_generic"} if generic else {"tm4tn16_w8x1"})
+    assert (kernels == {"lutconv_generic"}) if generic else ("lutconv_generic" not in kernels)
 
 
 def test_all_tile_variants_bit_identical():
