@@ -72,7 +72,35 @@ def workload_spec(name: str, lut_kind: str):
     if name == "r50":
         return dict(nodes=resnet.resnet50(lut, seed=0), batch=256, kind="imagenet", lut=lut_desc,
                     desc="ResNet-50 v1.5 224x224 (53 convs + 1x1 AxConv2D classifier), BN folded")
+    if name == "r62sweep":
+        return dict(nodes=resnet.cifar_resnet(10, sweep_luts()[0], seed=0), batch=1000, kind="cifar",
+                    lut="32 candidates: truncated_lut(mode, d) d=0..7 x {signed, unsigned} + 16 random_lut",
+                    desc="ResNet-62 CIFAR-10 multiplier sweep over 32 candidate tables (config 4)",
+                    sweep=True)
     raise SystemExit(f"unknown workload {name}")
+
+
+def sweep_luts():
+    """Config 4's 32 candidate multipliers."""
+    from paper_2002_09481_b200 import types as T
+
+    luts = [T.truncated_lut(m, d) for m in (T.Signedness.SIGNED, T.Signedness.UNSIGNED) for d in range(8)]
+    luts += [T.random_lut(np.random.default_rng(5000 + i), T.Signedness.SIGNED if i % 2 else T.Signedness.UNSIGNED)
+             for i in range(16)]
+    return luts
+
+
+def build_graphs(spec, name, world, rank, device):
+    """This rank's networks: one graph, or its shard of the candidate tables (config 4)."""
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200.dist import shard
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    if not spec.get("sweep"):
+        return [GpuGraph(spec["nodes"], device=device)], [0]
+    luts = sweep_luts()
+    mine = shard(len(luts), world, rank)
+    return [GpuGraph(resnet.cifar_resnet(10, luts[i], seed=0), device=device) for i in mine], mine
 
 
 def make_images(kind: str, n: int, seed: int):
@@ -192,7 +220,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="r8", choices=["r8", "r50", "r62"])
+    ap.add_argument("--workload", default="r8", choices=["r8", "r50", "r62", "r62sweep"])
     ap.add_argument("--lut", default="trunc2", choices=["trunc2", "exact", "random"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -243,19 +271,23 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2002_09481_b200.graph import GpuGraph
+    graphs, lut_ids = build_graphs(spec, args.workload, world, rank, local)
+    nets = len(graphs)
 
-    graph = GpuGraph(spec["nodes"], device=local)
-    imgs, labels = make_images(spec["kind"], batch, seed=1000 + rank)
+    def run_all(x, check=False, profile=None):
+        ys = [g.run(x, check=check, profile=profile) for g in graphs]
+        return ys
+
+    imgs, labels = make_images(spec["kind"], batch, seed=(1000 + rank) if not spec.get("sweep") else 1000)
     x_dev = torch.from_numpy(imgs).to(dev)
     x_host = torch.from_numpy(imgs).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     # warm-up (also prepares filters once: hoisted quantize_filters)
     for _ in range(args.warmup):
-        y = graph.run(x_dev, check=True)
+        ys = run_all(x_dev, check=True)
     torch.cuda.synchronize()
-    launches = graph.launches
+    launches = sum(g.launches for g in graphs)
 
     def barrier():
         if dist is not None:
@@ -272,7 +304,7 @@ def main():
         flush.zero_()  # write > L2 (126 MB) between timed steps
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        y = graph.run(x_dev, check=False, profile=profile)
+        ys = run_all(x_dev, profile=profile)
         e1.record()
         step_ms.append((e0, e1))
     barrier()
@@ -287,7 +319,9 @@ def main():
         r[0] += a.elapsed_time(b)
         r[1] += m
         r[2] += 1
-    graph.check_flags()
+    for g in graphs:
+        g.check_flags()
+    y = torch.stack([t.reshape(batch, -1) for t in ys])  # (nets, batch, classes)
 
     # ------------------------------------------------ end-to-end through the public API (host buffers)
     out_host = torch.empty(tuple(y.shape), dtype=torch.float32).pin_memory()
@@ -298,7 +332,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         xd = x_host.to(dev, non_blocking=True)
-        yd = graph.run(xd, check=False)
+        yd = torch.stack([t.reshape(batch, -1) for t in run_all(xd)])
         out_host.copy_(yd, non_blocking=True)
         e1.record()
         e1.synchronize()
@@ -310,17 +344,17 @@ def main():
     from paper_2002_09481_b200.dist import exchange_results
 
     t = torch.tensor([total_ms, e2e_total, conv_ms], dtype=torch.float64, device=dev)
-    logits = y.reshape(batch, -1)
-    pred = logits.argmax(1)
-    agree = (pred.cpu().numpy() == labels.astype(np.int64)).sum()
-    cnt = torch.tensor([int(agree), batch], dtype=torch.int64, device=dev)
+    logits = y  # (nets, batch, classes)
+    pred = logits.argmax(-1)
+    agree = (pred.cpu().numpy() == labels.astype(np.int64)[None, :]).sum(1)  # per network
+    cnt = torch.tensor(list(agree) + [batch * nets], dtype=torch.int64, device=dev)
     gathered, cnt, t = exchange_results(logits, cnt, t)
     total_ms, e2e_total, conv_ms_max = (float(v) for v in t.tolist())
     if rank != 0:
         dist.destroy_process_group()
         return
 
-    images = batch * world * args.steps
+    images = batch * nets * world * args.steps  # image x network evaluations
     gmacs = images * macs_img / (total_ms / 1e3) / 1e9
     e2e_gmacs = images * macs_img / (e2e_total / 1e3) / 1e9
 
@@ -353,14 +387,16 @@ def main():
         "vs_baseline_basis": "paper-derived GTX 1080 approx GMAC/s (BASELINE.md s1)" if args.workload in PAPER_GMACS else None,
         "dtype": "u8", "data": "synthetic",
         "config": {"workload": spec["desc"], "batch_per_gpu": batch, "lut": spec["lut"],
-                   "macs_per_image": macs_img, "parallelism": f"dp{world} (one range-batch per GPU)",
+                   "networks_per_gpu": nets, "macs_per_image": macs_img,
+                   "parallelism": (f"dp{world} (candidate tables sharded round-robin)" if spec.get("sweep")
+                                   else f"dp{world} (one range-batch per GPU)"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "roofline": roofline,
         "e2e": {"value": round(e2e_gmacs, 2), "unit": "GMAC/s", "images_per_s": round(images / (e2e_total / 1e3), 2),
                 "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4)},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
-        "agreement_with_labels": round(float(cnt[0]) / float(cnt[1]), 4),
+        "agreement_with_labels": round(float(cnt[:-1].sum()) / float(cnt[-1]), 4),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_rate(spec, macs_img, budget_s=args.cpu_budget)

@@ -140,6 +140,11 @@ typedef struct axb_conv_desc {
 
 int axb_conv2d_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);
 int axb_conv_variant_count(void);
+/* Depthwise approximate conv (config 5; the reference has no groups): channel c
+ * of the output == axconv2d on input channel c alone with the shared ranges.
+ * desc: cout == c; fcodes/fsum from axb_filters_prepare on the (kh,kw,1,c)
+ * view of the (kh,kw,c,1) filter (cs 16). */
+int axb_depthwise_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);
 const char *axb_conv_variant_name(int variant);
 
 /* ---- small-channel layers: explicit im2col of the codes (axconv.py:160-196) ----

@@ -84,6 +84,7 @@ SIGNATURES = {
                                     c_vp, c_vp, c_vp]),
     "axb_conv2d_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
     "axb_conv_variant_count": (c_int, []),
+    "axb_depthwise_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
     "axb_conv_variant_name": (ctypes.c_char_p, [c_int]),
     "axb_conv_im2col_kp": (c_i64, [c_i64, c_i64, c_i64]),
     "axb_im2col_pack": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,

@@ -122,6 +122,24 @@ __host__ __device__ inline void fill_bounds(axb_qparams &p, int is_signed, int r
         p.bound[u] = u == 0 ? -INFINITY : code_boundary(lo + u, p.scale, p.zero_point, is_signed, round_mode);
 }
 
+// ---- division by a runtime-constant divisor via a precomputed magic number
+// (round-up method): q = (umulhi(x, m) + x) >> l, exact for all 32-bit x.
+struct FastDiv {
+    uint32_t d, m, l;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d ? d : 1;
+    uint32_t l = 0;
+    while ((uint64_t(1) << l) < f.d) ++l;
+    f.l = l;
+    f.m = (uint32_t)(((uint64_t(1) << 32) * ((uint64_t(1) << l) - f.d)) / f.d + 1);
+    return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv &f) {
+    return (uint32_t)(((uint64_t)__umulhi(x, f.m) + x) >> f.l);
+}
+
 // ---- warp reductions
 __device__ __forceinline__ int32_t warp_min_i(int32_t v) {
 #pragma unroll

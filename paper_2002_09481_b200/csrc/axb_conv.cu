@@ -53,6 +53,7 @@ struct ConvK {
     int32_t ntn;
     int64_t ntiles;
     int32_t blk;  // 1: lanes = 32 consecutive pixels of a row; 4: lanes = a 4x8 pixel block
+    FastDiv fd_hw, fd_ow, fd_band;  // oh*ow, ow, 4*ow (M < 2^31 per launch)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -123,19 +124,20 @@ __device__ __forceinline__ EpiConst epi_const(const ConvK &p) {
 // 4x8 blocks so a warp instruction's 32 lanes are a compact pixel block (more
 // similar codes -> fewer LUT bank conflicts); needs oh % 4 == 0, ow % 8 == 0.
 __device__ __forceinline__ int64_t pixel_of(const ConvK &p, int64_t mt, int64_t &pix0) {
-    const int64_t hw = (int64_t)p.oh * p.ow;
-    const int64_t b = mt / hw;
-    const int64_t r = mt - b * hw;
+    const uint32_t hw = (uint32_t)p.oh * (uint32_t)p.ow;
+    const uint32_t b = fdiv((uint32_t)mt, p.fd_hw);
+    const uint32_t r = (uint32_t)mt - b * hw;
     int64_t oy, ox;
     if (p.blk == 4) {
-        const int64_t band = r / (4 * p.ow);
-        const int64_t rr = r - band * 4 * p.ow;
-        const int64_t bx = rr >> 5, s = rr & 31;
+        const uint32_t band = fdiv(r, p.fd_band);
+        const uint32_t rr = r - band * 4 * (uint32_t)p.ow;
+        const uint32_t bx = rr >> 5, s = rr & 31;
         oy = band * 4 + (s >> 3);
         ox = bx * 8 + (s & 7);
     } else {
-        oy = r / p.ow;
-        ox = r - oy * p.ow;
+        const uint32_t q = fdiv(r, p.fd_ow);
+        oy = q;
+        ox = r - q * (uint32_t)p.ow;
     }
     pix0 = (b * p.hp + oy * p.sh) * (int64_t)p.wp + ox * p.sw;
     return b * hw + oy * p.ow + ox;
@@ -559,7 +561,7 @@ static int launch_variant(int v, const ConvK &k, int sm_limit, cudaStream_t s) {
 // ones unless its tile count quantizes badly against the SM count.
 static int pick_variant(const ConvK &k) {
     if (k.coutp <= 16) return 4;   // tm4tn8_w8x2: 1024 x 16
-    if (k.coutp <= 32) return 5;   // tm4tn8_w4x4:  512 x 32
+    if (k.coutp <= 64) return 5;   // tm4tn8_w4x4:  512 x 32
     const int64_t sms = sm_count();
     auto eff = [&](int64_t bm, int64_t bn) {
         const int64_t tiles = ((k.M + bm - 1) / bm) * ((k.coutp + bn - 1) / bn);
@@ -629,6 +631,9 @@ int axb_conv2d_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
         if (order == 0) order = (d->oh % 4 == 0 && d->ow % 8 == 0) ? 4 : 1;
         if (order == 4 && (d->oh % 4 || d->ow % 8)) return set_error(AXB_E_VALUE, "4x8 pixel order needs oh%4==0, ow%8==0");
         k.blk = order == 4 ? 4 : 1;
+        k.fd_hw = make_fastdiv((uint32_t)(d->oh * d->ow));
+        k.fd_ow = make_fastdiv((uint32_t)d->ow);
+        k.fd_band = make_fastdiv((uint32_t)(4 * d->ow));
         for (int64_t b0 = 0; b0 < d->n; b0 += step) {
             const int64_t nb = (d->n - b0 < step) ? d->n - b0 : step;
             ConvK kc = k;

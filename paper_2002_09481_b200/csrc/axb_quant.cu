@@ -113,6 +113,7 @@ __device__ __forceinline__ int quant_exact(const QuantCtx &q, float x) {
 template <int G>
 __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restrict__ x, int64_t n, int64_t h, int64_t w,
                                                            int c, int64_t cs, int pt, int pl, int64_t hp, int64_t wp,
+                                                           FastDiv fd_hp, FastDiv fd_wp,
                                                            const axb_qparams *__restrict__ prm, int is_signed,
                                                            uint8_t *__restrict__ codes, int32_t *__restrict__ pixsum,
                                                            int32_t *d_flags) {
@@ -124,10 +125,11 @@ __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restri
     const int zpb = q.zp & 0xFF;
     int nonfinite = 0;
     auto group = [&](int64_t p, int64_t g, int32_t &s) -> uint32_t {
-        const int64_t xw = p % wp;
-        const int64_t t = p / wp;
-        const int64_t yh = t % hp;
-        const int64_t b = t / hp;
+        // npix < 2^32 (checked on the host): 32-bit magic-number division
+        const uint32_t t = fdiv((uint32_t)p, fd_wp);
+        const int64_t xw = (uint32_t)p - t * (uint32_t)wp;
+        const uint32_t b = fdiv(t, fd_hp);
+        const int64_t yh = t - b * (uint32_t)hp;
         const int64_t iy = yh - pt, ix = xw - pl;
         const int c0 = (int)g * 4;
         uint32_t word = 0;
@@ -248,18 +250,18 @@ __global__ void filters_sum_kernel(const uint16_t *__restrict__ fcodes, int64_t 
 // the exact row sum (= patch sum S_p, axconv.py:193).
 __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t *__restrict__ codes, int64_t n, int64_t hp,
                                                           int64_t wp, int64_t cs, int c, int kh, int kw, int sh,
-                                                          int sw, int dh, int dw, int64_t oh, int64_t ow, int kp,
-                                                          int is_signed, uint8_t *__restrict__ rows,
-                                                          int32_t *__restrict__ rowsum) {
+                                                          int sw, int dh, int dw, int64_t oh, int64_t ow, FastDiv fd_oh,
+                                                          FastDiv fd_ow, int kp, int is_signed,
+                                                          uint8_t *__restrict__ rows, int32_t *__restrict__ rowsum) {
     const int64_t total = n * oh * ow;
     const int K = kh * kw * c;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < total;
          r += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t ox = r % ow;
-        const int64_t t = r / ow;
-        const int64_t oy = t % oh;
-        const int64_t b = t / oh;
-        const uint8_t *base = codes + ((b * hp + oy * sh) * wp + ox * sw) * cs;
+        const uint32_t t = fdiv((uint32_t)r, fd_ow);
+        const int64_t ox = (uint32_t)r - t * (uint32_t)ow;
+        const uint32_t b = fdiv(t, fd_oh);
+        const int64_t oy = t - b * (uint32_t)oh;
+        const uint8_t *base = codes + (((int64_t)b * hp + oy * sh) * wp + ox * sw) * cs;
         int32_t s = 0;
         int k = 0, ky = 0, kx = 0, ci = 0;
         for (int g = 0; g < kp / 16; ++g) {
@@ -308,9 +310,10 @@ int axb_im2col_pack(const uint8_t *d_codes, int64_t n, int64_t hp, int64_t wp, i
     int64_t blocks = (rows + 255) / 256;
     const int64_t cap = (int64_t)sm_count() * 16;
     if (blocks > cap) blocks = cap;
-    im2col_pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_codes, n, hp, wp, cs, (int)c, kh, kw, sh, sw,
-                                                                       dh, dw, oh, ow, (int)kp, is_signed, d_rows,
-                                                                       d_rowsum);
+    if (rows >= (int64_t(1) << 32)) return set_error(AXB_E_VALUE, "im2col: more than 2^32 rows");
+    im2col_pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(
+        d_codes, n, hp, wp, cs, (int)c, kh, kw, sh, sw, dh, dw, oh, ow, make_fastdiv((uint32_t)oh),
+        make_fastdiv((uint32_t)ow), (int)kp, is_signed, d_rows, d_rowsum);
     return check_launch("im2col_pack");
 }
 
@@ -374,14 +377,16 @@ int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t 
     if (total == 0) return AXB_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cap = (int64_t)sm_count() * 16;
+    if (total >= (int64_t(1) << 32)) return set_error(AXB_E_VALUE, "quantize: more than 2^32 padded pixels");
+    const FastDiv fhp = make_fastdiv((uint32_t)hp), fwp = make_fastdiv((uint32_t)wp);
     const int64_t G = cs / 4;
     const int64_t work = (G <= 32 && (G & (G - 1)) == 0) ? total * G : total * 32;
     int64_t blocks = (work + 255) / 256;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
 #define AXB_QLAUNCH(GG)                                                                                             \
-    quantize_pad_kernel<GG><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, cs, pt, pl, hp, wp, d_params, is_signed, \
-                                                        d_codes, d_pixsum, d_flags)
+    quantize_pad_kernel<GG><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, cs, pt, pl, hp, wp, fhp, fwp, d_params, \
+                                                        is_signed, d_codes, d_pixsum, d_flags)
     switch (G) {
         case 4: AXB_QLAUNCH(4); break;
         case 8: AXB_QLAUNCH(8); break;

@@ -28,10 +28,15 @@ from .types import resolve_padding
 
 class ConvLayer:
     def __init__(self, filters, f_range, lut, geometry, bias=None, round_mode="half-away-from-zero",
-                 accumulator="exact64", device=None):
+                 accumulator="exact64", device=None, depthwise=False):
         self.lib = lib = _lib.load()
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
         f = np.ascontiguousarray(filters, dtype=np.float32)
+        self.depthwise = bool(depthwise)
+        if self.depthwise:  # (kh, kw, C, 1) -> the (kh, kw, 1, C) view: one input channel per output channel
+            if f.shape[3] != 1:
+                raise ValueError("depthwise filters must be (kh, kw, channels, 1)")
+            f = np.ascontiguousarray(f.reshape(f.shape[0], f.shape[1], 1, f.shape[2]))
         self.kh, self.kw, self.cin, self.cout = (int(v) for v in f.shape)
         self.geometry = geometry
         self.round = _lib.ROUND[getattr(round_mode, "value", round_mode)]
@@ -39,7 +44,7 @@ class ConvLayer:
         self.lut = device_lut(lut, self.device.index)
         self.sgn = int(self.lut.signed)
         self.cs = int(lib.axb_channel_stride(self.cin))
-        self.kp = int(lib.axb_conv_im2col_kp(self.cin, self.kh, self.kw))
+        self.kp = 0 if self.depthwise else int(lib.axb_conv_im2col_kp(self.cin, self.kh, self.kw))
         if self.kp:  # filters as (1, 1, K, cout): same (ky, kx, ci) flattening
             fk = (1, 1, self.kh * self.kw * self.cin, self.kp)
         else:
@@ -81,8 +86,9 @@ class ConvLayer:
         set_input_params() was called.  Returns (n,oh,ow,cout) fp32."""
         lib = self.lib
         n, h, w, c = (int(v) for v in x.shape)
-        if c != self.cin:
+        if c != (self.cout if self.depthwise else self.cin):
             raise ValueError(f"filter channels {self.cin} do not match input channels {c}")
+        in_cs = int(lib.axb_channel_stride(c))
         g = self.geometry
         pt, pb, pl, pr = resolve_padding(g, h, w, self.kh, self.kw)
         hp_, wp_ = h + pt + pb, w + pl + pr
@@ -99,9 +105,9 @@ class ConvLayer:
             _lib.check(lib.axb_coeffs_from_range(in_range_dev, self.sgn, self.round, self.params[0].data_ptr(), stream))
             self.launches += 1
         qflag = quant_flag if quant_flag is not None else out_flag
-        codes = torch.empty(n * hp_ * wp_ * self.cs, dtype=torch.uint8, device=self.device)
+        codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
         pixsum = torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
-        _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, self.cs, self.params[0].data_ptr(),
+        _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, self.params[0].data_ptr(),
                                         self.sgn, self.round, codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
         self.launches += 1
         d = _lib.ConvDesc()
@@ -116,7 +122,7 @@ class ConvLayer:
             d.n, d.hp, d.wp, d.cs, d.c = n, oh, ow, self.kp, self.kh * self.kw * c
             d.kh = d.kw = d.sh = d.sw = d.dh = d.dw = 1
         else:
-            d.n, d.hp, d.wp, d.cs, d.c = n, hp_, wp_, self.cs, c
+            d.n, d.hp, d.wp, d.cs, d.c = n, hp_, wp_, in_cs, c
             d.kh, d.kw = self.kh, self.kw
             d.sh, d.sw = g.strides
             d.dh, d.dw = g.dilations
@@ -143,7 +149,8 @@ class ConvLayer:
         if profile is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-        _lib.check(lib.axb_conv2d_lut(d, self.lut.handle, stream))
+        launch = lib.axb_depthwise_lut if self.depthwise else lib.axb_conv2d_lut
+        _lib.check(launch(d, self.lut.handle, stream))
         self.launches += 1
         if profile is not None:
             e1.record()

@@ -332,3 +332,28 @@ def test_exact_lut_control_full_size_layer():
         xp = F.pad(xc.permute(0, 3, 1, 2), (1, 1, 1, 1), value=float(z1))
         want = F.conv2d(xp, fc.permute(3, 2, 0, 1)).permute(0, 2, 3, 1)
         assert torch.equal(torch.from_numpy(acc).cuda().double(), want)
+
+
+@pytest.mark.parametrize("stride,shape,mode", [(1, (4, 28, 28, 32), O.SIGNED), (2, (4, 28, 28, 48), O.UNSIGNED),
+                                               (1, (2, 14, 14, 128), O.SIGNED)])
+def test_depthwise_matches_per_channel_oracle(stride, shape, mode):
+    """Config 5: depthwise approximate conv == per-channel axconv2d with shared ranges (bit-exact)."""
+    torch = _torch()
+    from paper_2002_09481_b200.layer import ConvLayer
+    from paper_2002_09481_b200.types import ConvGeometry
+
+    rng = np.random.default_rng(stride * 100 + shape[3])
+    x = np.maximum(rng.standard_normal(shape), 0).astype(np.float32)
+    f = (rng.standard_normal((3, 3, shape[3], 1)) * 0.3).astype(np.float32)
+    bias = (rng.standard_normal(shape[3]) * 0.05).astype(np.float32)
+    lut = O.random_lut(rng, mode)
+    ir, fr = (float(x.min()), float(x.max())), (float(f.min()), float(f.max()))
+    want = np.concatenate([O.axconv2d(x[..., c:c + 1], f[:, :, c:c + 1, :], ir, fr, lut, mode, padding="same",
+                                      strides=(stride, stride)) for c in range(shape[3])], axis=3)
+    want = (want + bias).astype(np.float32)
+    layer = ConvLayer(f, fr, _lut(lut, mode), ConvGeometry((stride, stride), (1, 1), "same"), bias=bias,
+                      depthwise=True)
+    layer.set_input_params(*ir)
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    y = layer.run(torch.from_numpy(x).cuda(), None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr())
+    assert bits_equal(y.cpu().numpy(), want)
