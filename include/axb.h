@@ -104,12 +104,12 @@ int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t 
                      int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags, void *stream);
 
 /* ---- filter preparation (once per layer) ---------------------------------- */
-/* d_f: HWCN fp32 (kh,kw,c,cout).  d_fcodes: (kpad, coutp) uint16 = 2*raw code
+/* d_f: HWCN fp32 (kh,kw,c,cout).  d_fcodes: (kpad, coutp) uint8 raw code bytes
  * (row k = (ky*kw + kx)*cs + ci; junk rows / columns = 0); d_fsum: int64[cout]. */
 int64_t axb_filter_kpad(int64_t kh, int64_t kw, int64_t cs);
 int64_t axb_filter_coutp(int64_t cout);
 int axb_filters_prepare(const float *d_f, int64_t kh, int64_t kw, int64_t c, int64_t cout, int64_t cs,
-                        const axb_qparams *d_params, int is_signed, int round_mode, uint16_t *d_fcodes,
+                        const axb_qparams *d_params, int is_signed, int round_mode, uint8_t *d_fcodes,
                         int64_t *d_fsum, int32_t *d_flags, void *stream);
 
 /* ---- K3: LUT implicit-GEMM convolution with fused epilogue ---------------- */
@@ -119,7 +119,7 @@ typedef struct axb_conv_desc {
     int64_t n, hp, wp, cs, c;
     int32_t kh, kw, sh, sw, dh, dw;
     int64_t oh, ow;
-    const uint16_t *fcodes; /* (kpad, coutp) from axb_filters_prepare               */
+    const uint8_t *fcodes;  /* (kpad, coutp) from axb_filters_prepare               */
     const int64_t *fsum;    /* (cout)                                               */
     int64_t cout, coutp, kpad;
     const axb_qparams *in_params; /* device */

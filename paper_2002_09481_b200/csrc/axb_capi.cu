@@ -257,7 +257,7 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
     uint8_t *codes = nullptr, *rows = nullptr;
     int32_t *pixsum = nullptr, *flags = nullptr, *rowsum = nullptr;
     axb_qparams *dp = nullptr;
-    uint16_t *fcodes = nullptr;
+    uint8_t *fcodes = nullptr;
     int64_t *fsum = nullptr;
     int rc = AXB_OK;
     auto fail = [&](int code, const char *msg) {
@@ -266,7 +266,7 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
     if (cudaMallocAsync(&codes, n * hp * wp * cs, s) != cudaSuccess ||
         cudaMallocAsync(&pixsum, n * hp * wp * 4, s) != cudaSuccess ||
         cudaMallocAsync(&flags, 8, s) != cudaSuccess || cudaMallocAsync(&dp, 2 * sizeof(axb_qparams), s) != cudaSuccess ||
-        cudaMallocAsync(&fcodes, kpad * coutp * 2, s) != cudaSuccess ||
+        cudaMallocAsync(&fcodes, kpad * coutp, s) != cudaSuccess ||
         cudaMallocAsync(&fsum, (cout > 0 ? cout : 1) * 8, s) != cudaSuccess ||
         (kp && (cudaMallocAsync(&rows, n * oh * ow * kp, s) != cudaSuccess ||
                 cudaMallocAsync(&rowsum, n * oh * ow * 4, s) != cudaSuccess))) {

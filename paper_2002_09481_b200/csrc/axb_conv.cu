@@ -36,7 +36,7 @@ struct ConvK {
     int32_t kh, kw, sh, sw, dh, dw;
     int32_t oh, ow;
     int64_t M;
-    const uint16_t *fcodes;
+    const uint8_t *fcodes;
     const int64_t *fsum;
     int32_t cout, coutp, kpad, nchunks, taps, K;
     const axb_qparams *inp;
@@ -190,11 +190,10 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     constexpr int BM = WM * 32 * TM;
     constexpr int BN = WN * TN;
     constexpr int ACT_STAGE = BM * 16;
-    constexpr int W_STAGE = 16 * BN * 2;
+    constexpr int W_STAGE = 16 * BN;  // 16 taps x BN channels, raw code bytes
     constexpr int NQ = BM / NT;  // activation rows per thread per chunk (one 16-byte cp.async each)
-    constexpr int WG = TN / 8;   // 16-byte weight groups per tap per warp
     static_assert(BM % NT == 0 && NQ >= 1, "tile/thread mismatch");
-    static_assert(2 * BN <= NT, "one weight piece per thread");
+    static_assert(BN <= NT, "one weight piece per thread");
     static_assert(TN % 8 == 0, "TN multiple of 8");
 
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -238,6 +237,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     // ---- producer state (runs kStages-1 iterations ahead of the consumer)
     int64_t ld_it = 0;
     int ld_kc = 0;
+    int ld_t = 0, ld_ci = 0;  // tap and channel offset of chunk ld_kc (cs % 16 == 0)
     int64_t ld_tile = blockIdx.x;
     int ld_n0 = 0;
     int32_t rowbase[NQ];
@@ -262,28 +262,32 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
             const int stage = (int)(ld_it % kStages);
             uint8_t *as = act_s + stage * ACT_STAGE;
             const int k0 = ld_kc * 16;
-            const int t = k0 / p.cs;
-            const int ci = k0 - t * p.cs;
-            const bool tv = t < p.taps;
-            const int off = tv ? tapoff_s[t] + ci : 0;
+            const bool tv = ld_t < p.taps;
+            const int off = tv ? tapoff_s[ld_t] + ld_ci : 0;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const bool v = tv && rowbase[q] >= 0;
                 const uint8_t *src = p.codes + (v ? (int64_t)rowbase[q] + off : 0);
                 cp_async16(as + (tid + q * NT) * 16, src, v ? 16 : 0);
             }
-            if (tid < 2 * BN) {
+            if (tid < BN) {  // 16 taps x BN bytes = BN 16-byte pieces
                 uint8_t *ws = w_s + stage * W_STAGE;
-                const int r = tid / (BN / 8);
-                const int col = (tid % (BN / 8)) * 8;
+                const int r = tid / (BN / 16);
+                const int col = (tid % (BN / 16)) * 16;
                 const int gcol = ld_n0 + col;
                 const bool v = gcol < p.coutp;
-                const uint16_t *src = p.fcodes + (v ? (int64_t)(k0 + r) * p.coutp + gcol : 0);
-                cp_async16(ws + (r * BN + col) * 2, src, v ? 16 : 0);
+                const uint8_t *src = p.fcodes + (v ? (int64_t)(k0 + r) * p.coutp + gcol : 0);
+                cp_async16(ws + r * BN + col, src, v ? 16 : 0);
             }
             ++ld_it;
+            ld_ci += 16;
+            if (ld_ci == p.cs) {
+                ld_ci = 0;
+                ++ld_t;
+            }
             if (++ld_kc == p.nchunks) {
                 ld_kc = 0;
+                ld_t = ld_ci = 0;
                 ld_tile += gridDim.x;
                 if (ld_it < total) set_load_tile(ld_tile);
             }
@@ -309,16 +313,13 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         load_next();
         const int stage = (int)(it % kStages);
         const uint8_t *as = act_s + stage * ACT_STAGE + (wm * 32 * TM + lane) * 16;
-        const uint8_t *ws = w_s + stage * W_STAGE + wn * TN * 2;
-        uint4 av[TM];
-#pragma unroll
-        for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const uint4 *>(as + i * 32 * 16);
+        const uint8_t *ws = w_s + stage * W_STAGE + wn * TN;
 
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {  // 4 taps per step, consumed as 2 pairs
-            uint32_t aw[TM];
+            uint32_t aw[TM];  // codes of taps 4q..4q+3 of this lane's TM pixels (one wavefront per load)
 #pragma unroll
-            for (int i = 0; i < TM; ++i) aw[i] = sel4(av[i], q);
+            for (int i = 0; i < TM; ++i) aw[i] = *reinterpret_cast<const uint32_t *>(as + i * 32 * 16 + q * 4);
 #pragma unroll
             for (int kk = 0; kk < 4; kk += 2) {
                 const int k0 = q * 4 + kk;
@@ -328,27 +329,36 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
                     a0[i] = __byte_perm(aw[i], 0, 0x4440u + kk) * 2u + lut_base;
                     a1[i] = __byte_perm(aw[i], 0, 0x4441u + kk) * 2u + lut_base;
                 }
-                uint4 wv0[WG], wv1[WG];
-#pragma unroll
-                for (int g = 0; g < WG; ++g) {
-                    wv0[g] = *reinterpret_cast<const uint4 *>(ws + k0 * BN * 2 + g * 16);
-                    wv1[g] = *reinterpret_cast<const uint4 *>(ws + (k0 + 1) * BN * 2 + g * 16);
+                uint32_t wv0[TN / 4], wv1[TN / 4];  // TN code bytes of taps k0, k0+1
+                if (TN == 16) {
+                    const uint4 x0 = *reinterpret_cast<const uint4 *>(ws + k0 * BN);
+                    const uint4 x1 = *reinterpret_cast<const uint4 *>(ws + (k0 + 1) * BN);
+                    wv0[0] = x0.x; wv0[1 % (TN / 4)] = x0.y; wv0[2 % (TN / 4)] = x0.z; wv0[3 % (TN / 4)] = x0.w;
+                    wv1[0] = x1.x; wv1[1 % (TN / 4)] = x1.y; wv1[2 % (TN / 4)] = x1.z; wv1[3 % (TN / 4)] = x1.w;
+                } else {
+                    const uint2 x0 = *reinterpret_cast<const uint2 *>(ws + k0 * BN);
+                    const uint2 x1 = *reinterpret_cast<const uint2 *>(ws + (k0 + 1) * BN);
+                    wv0[0] = x0.x; wv0[1] = x0.y;
+                    wv1[0] = x1.x; wv1[1] = x1.y;
                 }
 #pragma unroll
                 for (int j = 0; j < TN; ++j) {
-                    // u16 (2b) -> bytes 1..2: (2b) << 8 = b << 9 = byte offset of row b
-                    const uint32_t sel = (j & 1) ? 0x4324u : 0x4104u;
-                    const uint32_t b0 = __byte_perm(sel4(wv0[j >> 3], (j >> 1) & 3), 0, sel);
-                    const uint32_t b1 = __byte_perm(sel4(wv1[j >> 3], (j >> 1) & 3), 0, sel);
+                    // code byte b -> bits 8..15 (b << 8); address = 2*(b << 8) + (2a + base)
+                    const uint32_t sel = 0x4404u | ((uint32_t)(j & 3) << 4);
+                    const uint32_t b0 = __byte_perm(wv0[j >> 2], 0, sel);
+                    const uint32_t b1 = __byte_perm(wv1[j >> 2], 0, sel);
 #pragma unroll
                     for (int i = 0; i < TM; ++i) {
                         int32_t v0, v1;
+                        uint32_t ad0, ad1;  // one IMAD each: 2*(b<<8) + (2a + base)
+                        asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(ad0) : "r"(b0), "r"(a0[i]));
+                        asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(ad1) : "r"(b1), "r"(a1[i]));
                         if (SGN) {
-                            asm("ld.shared.s16 %0, [%1];" : "=r"(v0) : "r"(a0[i] + b0));
-                            asm("ld.shared.s16 %0, [%1];" : "=r"(v1) : "r"(a1[i] + b1));
+                            asm("ld.shared.s16 %0, [%1];" : "=r"(v0) : "r"(ad0));
+                            asm("ld.shared.s16 %0, [%1];" : "=r"(v1) : "r"(ad1));
                         } else {
-                            asm("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0[i] + b0));
-                            asm("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1[i] + b1));
+                            asm("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(ad0));
+                            asm("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(ad1));
                         }
                         acc[i][j] += v0 + v1;
                     }
@@ -475,9 +485,9 @@ __global__ void __launch_bounds__(256) lutconv_generic(const ConvK p) {
         for (int t = 0; t < p.taps; ++t) {
             const int64_t pix = pix0 + (small_taps ? tappix_s[t] : (t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw);
             const uint8_t *a = p.codes + pix * p.cs;
-            const uint16_t *f = p.fcodes + (int64_t)t * p.cs * p.coutp + c;
+            const uint8_t *f = p.fcodes + (int64_t)t * p.cs * p.coutp + c;
             for (int ci = 0; ci < p.c; ++ci) {
-                const uint32_t idx16 = ((uint32_t)(f[(int64_t)ci * p.coutp] >> 1) << 8) | a[ci];
+                const uint32_t idx16 = ((uint32_t)f[(int64_t)ci * p.coutp] << 8) | a[ci];
                 const uint16_t raw = __ldg(p.lut + idx16);
                 A += SGN ? (int64_t)(int16_t)raw : (int64_t)raw;
             }
@@ -515,7 +525,7 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 template <int TM, int TN, int WM, int WN, bool SGN>
 static int launch_fast(const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WM * 32 * TM, BN = WN * TN;
-    const size_t smem = kLutBytes + kStages * (BM * 16 + 16 * BN * 2) + 2 * kMaxTaps * 4 + BN * 12 + 8 + 16;
+    const size_t smem = kLutBytes + kStages * (BM * 16 + 16 * BN) + 2 * kMaxTaps * 4 + BN * 12 + 8 + 16;
     auto fn = lutconv_fast<TM, TN, WM, WN, SGN>;
     static int configured_dev = -1;  // one per instantiation
     int dev = 0;

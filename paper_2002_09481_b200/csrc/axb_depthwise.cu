@@ -24,7 +24,7 @@ struct DwK {
     int64_t n, hp, wp, cs;
     int32_t c, kh, kw, sh, sw, dh, dw;
     int64_t oh, ow;
-    const uint16_t *fcodes;  // rows t*16, columns c (2*code)
+    const uint8_t *fcodes;  // rows t*16, columns c (raw code bytes)
     const int64_t *fsum;
     int32_t coutp;
     const axb_qparams *inp, *fp;
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(1024, 1) depthwise_lut_kernel(const DwK p) {
             for (int kx = 0; kx < p.kw; ++kx) {
                 const int t = ky * p.kw + kx;
                 const uint32_t a = __ldg(base + ((int64_t)ky * p.dh * p.wp + kx * p.dw) * p.cs);
-                const uint32_t bc = __ldg(p.fcodes + (int64_t)t * 16 * p.coutp + c) >> 1;
+                const uint32_t bc = __ldg(p.fcodes + (int64_t)t * 16 * p.coutp + c);
                 const uint16_t raw = lut_s[(bc << 8) | a];
                 A += p.sgn ? (int32_t)(int16_t)raw : (int32_t)raw;
                 sp += p.sgn ? (int32_t)(int8_t)a : (int32_t)a;

@@ -193,11 +193,10 @@ __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restri
 }
 
 // ---------------------------------------------------------------- filters
-// HWCN fp32 -> (kpad, coutp) uint16 = 2 * raw code byte (pre-scaled so the conv
-// kernel builds b<<9 with one PRMT); row k = (ky*kw + kx)*cs + ci.
+// HWCN fp32 -> (kpad, coutp) uint8 raw code bytes; row k = (ky*kw + kx)*cs + ci.
 __global__ void filters_codes_kernel(const float *__restrict__ f, int64_t kh, int64_t kw, int64_t c, int64_t cout,
                                      int64_t cs, int64_t kpad, int64_t coutp, const axb_qparams *__restrict__ prm,
-                                     int is_signed, int round_mode, uint16_t *__restrict__ fcodes, int32_t *d_flags) {
+                                     int is_signed, int round_mode, uint8_t *__restrict__ fcodes, int32_t *d_flags) {
     const double scale = prm->scale;
     const int zp = prm->zero_point;
     const int64_t total = kpad * coutp;
@@ -207,12 +206,12 @@ __global__ void filters_codes_kernel(const float *__restrict__ f, int64_t kh, in
         const int64_t co = i % coutp;
         const int64_t k = i / coutp;
         const int64_t tap = k / cs, ci = k % cs;
-        uint16_t v = 0;
+        uint8_t v = 0;
         if (co < cout && tap < kh * kw && ci < c) {
             const float fv = f[(tap * c + ci) * cout + co];  // HWCN flat: ((ky*kw+kx)*c+ci)*cout+co
             nonfinite |= !isfinite(fv);
             const int q = quantize_one(fv, scale, zp, is_signed, round_mode);
-            v = (uint16_t)((q & 0xFF) << 1);
+            v = (uint8_t)(q & 0xFF);
         }
         fcodes[i] = v;
     }
@@ -220,7 +219,7 @@ __global__ void filters_codes_kernel(const float *__restrict__ f, int64_t kh, in
 }
 
 // S_f[co] = sum of code values over the real taps (axconv.py:207), int64 + overflow flag
-__global__ void filters_sum_kernel(const uint16_t *__restrict__ fcodes, int64_t kh, int64_t kw, int64_t c,
+__global__ void filters_sum_kernel(const uint8_t *__restrict__ fcodes, int64_t kh, int64_t kw, int64_t c,
                                    int64_t cout, int64_t cs, int64_t coutp, int is_signed, int64_t *fsum,
                                    int32_t *d_flags) {
     const int64_t co = blockIdx.x;
@@ -228,7 +227,7 @@ __global__ void filters_sum_kernel(const uint16_t *__restrict__ fcodes, int64_t 
     const int64_t taps = kh * kw;
     for (int64_t k = threadIdx.x; k < taps * c; k += blockDim.x) {
         const int64_t tap = k / c, ci = k % c;
-        const int raw = fcodes[(tap * cs + ci) * coutp + co] >> 1;
+        const int raw = fcodes[(tap * cs + ci) * coutp + co];
         s += is_signed ? (int)(int8_t)raw : raw;
     }
     __shared__ long long red[256];
@@ -402,7 +401,7 @@ int64_t axb_filter_kpad(int64_t kh, int64_t kw, int64_t cs) { return (kh * kw * 
 int64_t axb_filter_coutp(int64_t cout) { return (cout + 15) / 16 * 16; }
 
 int axb_filters_prepare(const float *d_f, int64_t kh, int64_t kw, int64_t c, int64_t cout, int64_t cs,
-                        const axb_qparams *d_params, int is_signed, int round_mode, uint16_t *d_fcodes,
+                        const axb_qparams *d_params, int is_signed, int round_mode, uint8_t *d_fcodes,
                         int64_t *d_fsum, int32_t *d_flags, void *stream) {
     if (cs != axb_channel_stride(c)) return set_error(AXB_E_VALUE, "channel stride mismatch");
     const int64_t kpad = axb_filter_kpad(kh, kw, cs), coutp = axb_filter_coutp(cout);

@@ -58,7 +58,7 @@ class ConvLayer:
         _lib.check(lib.axb_coeffs_host(float(f_range[0]), float(f_range[1]), self.sgn, self.round, hp))
         _lib.check(lib.axb_params_upload(hp, self.params[1].data_ptr(), stream))
         fd = torch.from_numpy(f).to(self.device)
-        self.fcodes = torch.empty(self.kpad * self.coutp, dtype=torch.int16, device=self.device)
+        self.fcodes = torch.empty(self.kpad * self.coutp, dtype=torch.uint8, device=self.device)
         self.fsum = torch.empty(max(self.cout, 1), dtype=torch.int64, device=self.device)
         fl = torch.zeros(1, dtype=torch.int32, device=self.device)
         _lib.check(lib.axb_filters_prepare(fd.data_ptr(), fk[0], fk[1], fk[2], self.cout, fk[3],
