@@ -111,7 +111,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # AXB_LIB_PATH: load an alternative in-tree build (A/B kernel experiments)
+    p = Path(path) if path else Path(os.environ.get("AXB_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise AxbError(
             f"{p} is missing: the CUDA extension is not built "

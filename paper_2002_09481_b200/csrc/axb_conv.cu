@@ -54,6 +54,7 @@ struct ConvK {
     int64_t ntiles;
     int32_t blk;  // 1: lanes = 32 consecutive pixels of a row; 4: lanes = a 4x8 pixel block
     FastDiv fd_hw, fd_ow, fd_band;  // oh*ow, ow, 4*ow (M < 2^31 per launch)
+    int32_t sp_inloop;  // 1: patch sums accumulated in the chunk loop (dp4a), 0: gathered in the epilogue
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -296,10 +297,14 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     };
 
     int32_t acc[TM][TN];
+    int32_t spa[TM];  // in-loop patch sums (sp_inloop)
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TM; ++i) {
+        spa[i] = 0;
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0;
+    }
+    const bool sp_inloop = p.sp_inloop != 0;
 
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s) load_next();
@@ -320,6 +325,12 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
             uint32_t aw[TM];  // codes of taps 4q..4q+3 of this lane's TM pixels (one wavefront per load)
 #pragma unroll
             for (int i = 0; i < TM; ++i) aw[i] = *reinterpret_cast<const uint32_t *>(as + i * 32 * 16 + q * 4);
+            if (sp_inloop) {  // S_p += sum of the 4 code values (junk codes are raw 0 -> value 0)
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+                    spa[i] = SGN ? __dp4a((int)aw[i], 0x01010101, spa[i])
+                                 : (int32_t)__dp4a(aw[i], 0x01010101u, (uint32_t)spa[i]);
+            }
 #pragma unroll
             for (int kk = 0; kk < 4; kk += 2) {
                 const int k0 = q * 4 + kk;
@@ -390,8 +401,11 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
             if (mt < p.M) {
                 int64_t pix0;
                 const int64_t m = pixel_of(p, mt, pix0);  // NHWC output pixel + its window origin
-                int64_t sp = 0;                            // S_p (axconv.py:193)
-                for (int t = 0; t < p.taps; ++t) sp += p.pixsum[pix0 + tappix_s[t]];
+                int64_t sp = spa[i];                       // S_p (axconv.py:193)
+                if (!sp_inloop) {
+                    sp = 0;
+                    for (int t = 0; t < p.taps; ++t) sp += p.pixsum[pix0 + tappix_s[t]];
+                }
                 psum_ovf |= (sp > INT32_MAX || sp < INT32_MIN);
                 const int64_t pz = -e.zp2 * sp;
                 float y[TN];
@@ -445,6 +459,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
                     }
                 }
             }
+            spa[i] = 0;
 #pragma unroll
             for (int j = 0; j < TN; ++j) acc[i][j] = 0;
         }
@@ -644,6 +659,8 @@ int axb_conv2d_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
         k.fd_hw = make_fastdiv((uint32_t)(d->oh * d->ow));
         k.fd_ow = make_fastdiv((uint32_t)d->ow);
         k.fd_band = make_fastdiv((uint32_t)(4 * d->ow));
+        // short K: the epilogue's per-pixel tap gather dominates -> sum codes in the loop instead
+        k.sp_inloop = d->kpad <= 512 ? 1 : 0;
         for (int64_t b0 = 0; b0 < d->n; b0 += step) {
             const int64_t nb = (d->n - b0 < step) ? d->n - b0 : step;
             ConvK kc = k;
