@@ -227,7 +227,6 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         for (int q = 0; q < 4; ++q) bulk_g2s(smem + q * 32768, p.lut + q * 16384, 32768, bar);
     }
 
-    const EpiConst e = epi_const(p);
     float tmin = INFINITY, tmax = -INFINITY;
     int nonfinite = 0, psum_ovf = 0;
     const uint32_t lut_base = smem_u32(smem);
@@ -320,16 +319,37 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         const uint8_t *as = act_s + stage * ACT_STAGE + (wm * 32 * TM + lane) * 16;
         const uint8_t *ws = w_s + stage * W_STAGE + wn * TN;
 
+        // All 16 taps of this lane's TM pixel rows in one LDS.128 each: a quarter-warp
+        // reads 8 adjacent 16-byte rows = 128 contiguous bytes, so 4 wavefronts per row
+        // per chunk (four 32-bit loads at a 16-byte lane stride would cost 4 each).
+        uint4 av[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const uint4 *>(as + i * 32 * 16);
+        if (sp_inloop) {  // S_p += sum of the 16 code values (junk codes are raw 0 -> value 0)
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                if (SGN) {
+                    int s = __dp4a((int)av[i].x, 0x01010101, spa[i]);
+                    s = __dp4a((int)av[i].y, 0x01010101, s);
+                    s = __dp4a((int)av[i].z, 0x01010101, s);
+                    spa[i] = __dp4a((int)av[i].w, 0x01010101, s);
+                } else {
+                    uint32_t s = __dp4a(av[i].x, 0x01010101u, (uint32_t)spa[i]);
+                    s = __dp4a(av[i].y, 0x01010101u, s);
+                    s = __dp4a(av[i].z, 0x01010101u, s);
+                    spa[i] = (int32_t)__dp4a(av[i].w, 0x01010101u, s);
+                }
+            }
+        }
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {  // 4 taps per step, consumed as 2 pairs
-            uint32_t aw[TM];  // codes of taps 4q..4q+3 of this lane's TM pixels (one wavefront per load)
+            uint32_t aw[TM];  // codes of taps 4q..4q+3 of this lane's TM pixels
 #pragma unroll
-            for (int i = 0; i < TM; ++i) aw[i] = *reinterpret_cast<const uint32_t *>(as + i * 32 * 16 + q * 4);
-            if (sp_inloop) {  // S_p += sum of the 4 code values (junk codes are raw 0 -> value 0)
-#pragma unroll
-                for (int i = 0; i < TM; ++i)
-                    spa[i] = SGN ? __dp4a((int)aw[i], 0x01010101, spa[i])
-                                 : (int32_t)__dp4a(aw[i], 0x01010101u, (uint32_t)spa[i]);
+            for (int i = 0; i < TM; ++i) {
+                aw[i] = av[i].x;  // rotate the row so word 0 is always the current step's
+                av[i].x = av[i].y;
+                av[i].y = av[i].z;
+                av[i].z = av[i].w;
             }
 #pragma unroll
             for (int kk = 0; kk < 4; kk += 2) {
@@ -382,6 +402,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         // In this kernel kpad <= 32768, so |A| < 2^31: WRAP32 and SATURATE32 are the
         // identity on the exact sum (axconv.py:128-133) and A = acc - junk exactly.
         c_kc = 0;
+        const EpiConst e = epi_const(p);  // re-read per tile (keeps ~10 registers out of the main loop)
         const int64_t m0 = (c_tile / p.ntn) * BM;
         const int n0 = (int)(c_tile % p.ntn) * BN;
         c_tile += gridDim.x;
