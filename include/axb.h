@@ -15,6 +15,7 @@
  *   axb_coeffs_from_range   <- quantizer.py:98-117 compute_coeffs (device-side, no host sync)
  *   axb_coeffs_host         <- quantizer.py:98-117 compute_coeffs (host scalars)
  *   axb_quantize_pad        <- quantizer.py:120-131 quantize_values + axconv.py:181-189 zp padding
+ *   axb_quantize_pad_range  <- the two above fused (coefficients of a device range, then quantize)
  *   axb_filters_prepare     <- axconv.py:199-210  quantize_filters (K x Cout codes + S_f)
  *   axb_conv2d_lut          <- axconv.py:213-257  approx_gemm/_lut_matmul (:136-146) + im2cols
  *                              (:160-196, implicit) + graph.py:268-277 bias / ReLU epilogue
@@ -61,7 +62,7 @@ extern "C" {
 typedef struct axb_qparams {
     double scale;
     int32_t zero_point;
-    int32_t valid; /* 1 once computed */
+    int32_t valid; /* 1 once computed; 2 = scale/zero_point only, bound[] unset (axb_quantize_pad_range) */
     float bound[256];
 } axb_qparams;
 
@@ -102,6 +103,13 @@ int64_t axb_channel_stride(int64_t c);
 int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
                      int32_t pl, int32_t pr, int64_t cs, const axb_qparams *d_params, int is_signed,
                      int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags, void *stream);
+/* Same, with compute_coeffs (quantizer.py:98-117) of the device range d_range done in the
+ * kernel prologue (no separate coefficient launch); the parameters used are written to
+ * d_params_out for the conv epilogue. */
+int axb_quantize_pad_range(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
+                           int32_t pl, int32_t pr, int64_t cs, const int32_t *d_range, int is_signed, int round_mode,
+                           axb_qparams *d_params_out, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags,
+                           void *stream);
 
 /* ---- filter preparation (once per layer) ---------------------------------- */
 /* d_f: HWCN fp32 (kh,kw,c,cout).  d_fcodes: (kpad, coutp) uint8 raw code bytes

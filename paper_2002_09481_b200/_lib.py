@@ -78,6 +78,8 @@ SIGNATURES = {
     "axb_channel_stride": (c_i64, [c_i64]),
     "axb_quantize_pad": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i64,
                                  c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_vp]),
+    "axb_quantize_pad_range": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i64,
+                                       c_vp, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "axb_filter_kpad": (c_i64, [c_i64, c_i64, c_i64]),
     "axb_filter_coutp": (c_i64, [c_i64]),
     "axb_filters_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_int, c_int, c_vp,

@@ -153,17 +153,37 @@ __device__ __forceinline__ int32_t warp_max_i(int32_t v) {
 }
 
 // Block-level range accumulation of a thread's running [min,max] (ordered ints) + nonfinite.
+// Block-level min/max/non-finite commit: warp shuffles, then one warp combines
+// the per-warp results and ONE lane issues the atomics (one atomicMin/Max pair
+// per CTA, not per warp -- same-address atomics serialise in L2).  Must be
+// called by every thread of the block (it contains a barrier).
 __device__ __forceinline__ void range_commit(int32_t tmin, int32_t tmax, int nonfinite, int32_t *d_range,
                                              int32_t *d_flags, int32_t flag_bit) {
+    __shared__ int32_t s_min[32], s_max[32], s_nf[32];
     tmin = warp_min_i(tmin);
     tmax = warp_max_i(tmax);
     const unsigned nf = __ballot_sync(0xffffffffu, nonfinite);
-    if ((threadIdx.x & 31) == 0) {
-        if (d_range) {
-            if (tmin != INT32_MAX) atomicMin(d_range, tmin);
-            if (tmax != INT32_MIN) atomicMax(d_range + 1, tmax);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = (blockDim.x + 31) >> 5;
+    if (lane == 0) {
+        s_min[w] = tmin;
+        s_max[w] = tmax;
+        s_nf[w] = nf != 0;
+    }
+    __syncthreads();
+    if (w == 0) {
+        tmin = lane < nw ? s_min[lane] : INT32_MAX;
+        tmax = lane < nw ? s_max[lane] : INT32_MIN;
+        const unsigned anf = __ballot_sync(0xffffffffu, lane < nw && s_nf[lane]);
+        tmin = warp_min_i(tmin);
+        tmax = warp_max_i(tmax);
+        if (lane == 0) {
+            if (d_range) {
+                if (tmin != INT32_MAX) atomicMin(d_range, tmin);
+                if (tmax != INT32_MIN) atomicMax(d_range + 1, tmax);
+            }
+            if (anf && d_flags) atomicOr(d_flags, flag_bit);
         }
-        if (nf && d_flags) atomicOr(d_flags, flag_bit);
     }
 }
 

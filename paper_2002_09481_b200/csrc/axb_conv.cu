@@ -27,7 +27,21 @@
 namespace axb {
 
 constexpr int kMaxTaps = 256;
-constexpr int kStages = 4;
+constexpr int kSmemBudget = 232448;  // 227 KiB opt-in dynamic shared memory per CTA
+constexpr int kChunkGroup = 2;       // 16-tap sub-chunks consumed per barrier period
+
+// bytes of shared memory besides the activation/weight ring
+// (+512: range_commit's static shared scratch)
+__host__ __device__ constexpr int fixed_smem(int BN) { return kLutBytes + 2 * kMaxTaps * 4 + 2 * BN * 12 + 32 + 512; }
+// ring depth in groups of kChunkGroup sub-chunks (4 when it fits, at least 2 = double buffering)
+__host__ __device__ constexpr int ring_groups(int BM, int BN) {
+    return (kSmemBudget - fixed_smem(BN)) / (kChunkGroup * (BM * 16 + 16 * BN)) >= 4   ? 4
+           : (kSmemBudget - fixed_smem(BN)) / (kChunkGroup * (BM * 16 + 16 * BN)) >= 3 ? 3
+                                                                                         : 2;
+}
+__host__ __device__ constexpr int fast_smem(int BM, int BN) {
+    return fixed_smem(BN) + ring_groups(BM, BN) * kChunkGroup * (BM * 16 + 16 * BN);
+}
 
 struct ConvK {
     const uint8_t *codes;
@@ -182,9 +196,11 @@ __device__ __forceinline__ void track(float y, float &fmin, float &fmax, int &no
 // ---------------------------------------------------------------- fast kernel
 // Persistent CTA (one per SM, the LUT takes 128 KiB of its shared memory).
 // The CTA walks its tiles (tile = blockIdx.x + j*gridDim.x) and their 16-tap
-// chunks as ONE continuous stream of iterations, so the cp.async ring keeps
-// prefetching the next tile's first chunks while the current tile finishes
-// and runs its epilogue (no per-tile pipeline fill / drain).
+// sub-chunks as ONE continuous stream, so the cp.async ring keeps prefetching
+// the next tile's first sub-chunks while the current tile finishes and runs
+// its epilogue (no per-tile pipeline fill / drain).  The stream is consumed in
+// groups of kChunkGroup sub-chunks per barrier period (one cp.async wait +
+// __syncthreads + one producer step per group), through a ring of NG groups.
 template <int TM, int TN, int WM, int WN, bool SGN>
 __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     constexpr int NT = WM * WN * 32;
@@ -192,6 +208,10 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     constexpr int BN = WN * TN;
     constexpr int ACT_STAGE = BM * 16;
     constexpr int W_STAGE = 16 * BN;  // 16 taps x BN channels, raw code bytes
+    constexpr int G = kChunkGroup;
+    constexpr int NG = ring_groups(BM, BN);
+    constexpr int SLOTS = G * NG;
+    static_assert(fast_smem(BM, BN) <= kSmemBudget, "tile variant exceeds shared memory");
     constexpr int NQ = BM / NT;  // activation rows per thread per chunk (one 16-byte cp.async each)
     static_assert(BM % NT == 0 && NQ >= 1, "tile/thread mismatch");
     static_assert(BN <= NT, "one weight piece per thread");
@@ -199,12 +219,12 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
 
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *act_s = smem + kLutBytes;
-    uint8_t *w_s = act_s + kStages * ACT_STAGE;
-    int32_t *tapoff_s = reinterpret_cast<int32_t *>(w_s + kStages * W_STAGE);
+    uint8_t *w_s = act_s + SLOTS * ACT_STAGE;
+    int32_t *tapoff_s = reinterpret_cast<int32_t *>(w_s + SLOTS * W_STAGE);
     int32_t *tappix_s = tapoff_s + kMaxTaps;
-    int64_t *ep_cc = reinterpret_cast<int64_t *>(tappix_s + kMaxTaps);  // BN per-channel constants
-    float *ep_bias = reinterpret_cast<float *>(ep_cc + BN);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(ep_bias + BN + (BN & 1));
+    int64_t *ep_cc_s = reinterpret_cast<int64_t *>(tappix_s + kMaxTaps);  // 2 x BN per-channel constants
+    float *ep_bias_s = reinterpret_cast<float *>(ep_cc_s + 2 * BN);          // 2 x BN (by tile parity)
+    uint64_t *bar = reinterpret_cast<uint64_t *>(ep_bias_s + 2 * BN);
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -234,7 +254,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     const int64_t my_tiles = (p.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int64_t total = my_tiles * p.nchunks;
 
-    // ---- producer state (runs kStages-1 iterations ahead of the consumer)
+    // ---- producer state (runs NG-1 groups ahead of the consumer)
     int64_t ld_it = 0;
     int ld_kc = 0;
     int ld_t = 0, ld_ci = 0;  // tap and channel offset of chunk ld_kc (cs % 16 == 0)
@@ -259,7 +279,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     set_load_tile(ld_tile);
     auto load_next = [&]() {
         if (ld_it < total) {
-            const int stage = (int)(ld_it % kStages);
+            const int stage = (int)(ld_it % SLOTS);
             uint8_t *as = act_s + stage * ACT_STAGE;
             const int k0 = ld_kc * 16;
             const bool tv = ld_t < p.taps;
@@ -292,6 +312,10 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
                 if (ld_it < total) set_load_tile(ld_tile);
             }
         }
+    };
+    auto load_group = [&]() {
+#pragma unroll
+        for (int g = 0; g < G; ++g) load_next();
         cp_async_commit();
     };
 
@@ -306,16 +330,21 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     const bool sp_inloop = p.sp_inloop != 0;
 
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) load_next();
+    for (int s = 0; s < NG - 1; ++s) load_group();
     mbar_wait(bar, 0);
 
     int c_kc = 0;
     int64_t c_tile = blockIdx.x;
-    for (int64_t it = 0; it < total; ++it) {
-        cp_async_wait<kStages - 2>();
-        __syncthreads();
-        load_next();
-        const int stage = (int)(it % kStages);
+    int ep_par = 0;  // epilogue constant buffer (alternates per tile)
+    for (int64_t it0 = 0; it0 < total; it0 += G) {
+      cp_async_wait<NG - 2>();
+      __syncthreads();
+      load_group();
+#pragma unroll 1
+      for (int g = 0; g < G; ++g) {
+        const int64_t it = it0 + g;
+        if (it >= total) break;
+        const int stage = (int)(it % SLOTS);
         const uint8_t *as = act_s + stage * ACT_STAGE + (wm * 32 * TM + lane) * 16;
         const uint8_t *ws = w_s + stage * W_STAGE + wn * TN;
 
@@ -406,6 +435,9 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
         const int64_t m0 = (c_tile / p.ntn) * BM;
         const int n0 = (int)(c_tile % p.ntn) * BN;
         c_tile += gridDim.x;
+        int64_t *ep_cc = ep_cc_s + ep_par * BN;  // double-buffered: a barrier period may hold two epilogues
+        float *ep_bias = ep_bias_s + ep_par * BN;
+        ep_par ^= 1;
         if (tid < BN) {  // per-channel constants: K*zp1*zp2 - zp1*S_f[c] - junk, bias
             const int c = n0 + tid;
             ep_cc[tid] = c < p.cout ? e.kzz - e.zp1 * p.fsum[c] - e.junk : 0;
@@ -484,7 +516,8 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
 #pragma unroll
             for (int j = 0; j < TN; ++j) acc[i][j] = 0;
         }
-    }
+      }  // sub-chunk g
+    }    // group it0
     cp_async_wait<0>();
     const bool any = tmin <= tmax;
     range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
@@ -561,7 +594,7 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 template <int TM, int TN, int WM, int WN, bool SGN>
 static int launch_fast(const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WM * 32 * TM, BN = WN * TN;
-    const size_t smem = kLutBytes + kStages * (BM * 16 + 16 * BN) + 2 * kMaxTaps * 4 + BN * 12 + 8 + 16;
+    const size_t smem = fast_smem(BM, BN) - 512;  // dynamic part (range_commit scratch is static)
     auto fn = lutconv_fast<TM, TN, WM, WN, SGN>;
     static int configured_dev = -1;  // one per instantiation
     int dev = 0;

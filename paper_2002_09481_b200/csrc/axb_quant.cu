@@ -22,16 +22,38 @@ __global__ void __launch_bounds__(256) range_kernel(const float *__restrict__ x,
     if (aligned) {
         const int64_t n4 = n >> 2;
         const float4 *x4 = reinterpret_cast<const float4 *>(x);
-        for (int64_t i = tid; i < n4; i += stride) {
+        // 4 independent 16-byte loads in flight per thread per iteration
+        float fmn = INFINITY, fmx = -INFINITY;
+        int64_t i = tid;
+        for (; i + 3 * stride < n4; i += 4 * stride) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(x4 + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    nonfinite |= !(fabsf(e[q]) <= 3.402823466e38f);
+                    fmn = fminf(fmn, e[q]);
+                    fmx = fmaxf(fmx, e[q]);
+                }
+            }
+        }
+        for (; i < n4; i += stride) {
             const float4 v = __ldg(x4 + i);
             const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                nonfinite |= !isfinite(e[q]);
-                const int32_t o = f2ord(e[q]);
-                tmin = min(tmin, o);
-                tmax = max(tmax, o);
+                nonfinite |= !(fabsf(e[q]) <= 3.402823466e38f);
+                fmn = fminf(fmn, e[q]);
+                fmx = fmaxf(fmx, e[q]);
             }
+        }
+        // fminf/fmaxf ignore NaN (flagged above); -0/+0 order is irrelevant to compute_coeffs
+        if (fmn <= fmx) {
+            tmin = min(tmin, f2ord(fmn));
+            tmax = max(tmax, f2ord(fmx));
         }
         head = n4 << 2;
     }
@@ -85,8 +107,11 @@ __global__ void params_set_kernel(axb_qparams p, axb_qparams *out) {
 // or a warp per pixel (G == 0: cs > 128 or not a power of two).
 struct QuantCtx {
     float bnd[257];
+    double scale;
     float inv, zpo;
     int lo, zp;
+    int table;  // bnd[] valid (axb_quantize_pad); else exact fp64 quantize_one for ties (axb_quantize_pad_range)
+    int sgn, round;
 };
 
 __device__ __forceinline__ void quant_ctx_load(QuantCtx &q, const axb_qparams *prm, int is_signed) {
@@ -97,6 +122,34 @@ __device__ __forceinline__ void quant_ctx_load(QuantCtx &q, const axb_qparams *p
         q.zp = prm->zero_point;
         q.inv = (float)(1.0 / prm->scale);
         q.zpo = (float)(prm->zero_point - q.lo);
+        q.table = 1;
+    }
+    __syncthreads();
+}
+
+// Context computed in-kernel from a device range (compute_coeffs, quantizer.py:98-117):
+// scale and zero point only -- no boundary table; the rare elements the fp32 estimate
+// cannot decide go through the exact fp64 quantize_one.  Block 0 publishes scale and
+// zero point for the conv epilogue (this replaces a coeffs_kernel launch).
+__device__ __forceinline__ void quant_ctx_from_range(QuantCtx &q, const int32_t *d_range, int is_signed,
+                                                     int round_mode, axb_qparams *p_out) {
+    if (threadIdx.x == 0) {
+        const float mn = ord2f(d_range[0]);
+        const float mx = ord2f(d_range[1]);
+        const axb_qparams p = coeffs((double)mn, (double)mx, is_signed, round_mode);
+        q.lo = is_signed ? -128 : 0;
+        q.zp = p.zero_point;
+        q.scale = p.scale;
+        q.inv = (float)(1.0 / p.scale);
+        q.zpo = (float)(p.zero_point - q.lo);
+        q.table = 0;
+        q.sgn = is_signed;
+        q.round = round_mode;
+        if (blockIdx.x == 0) {
+            p_out->scale = p.scale;
+            p_out->zero_point = p.zero_point;
+            p_out->valid = 2;  // parameters only (bound[] not filled)
+        }
     }
     __syncthreads();
 }
@@ -110,67 +163,101 @@ __device__ __forceinline__ int quant_exact(const QuantCtx &q, float x) {
     return q.lo + u;
 }
 
+// Offset u = code - lo for the two round-to-nearest modes without touching the
+// table in the common case.  uf = fl(x*fl(1/scale) + (zp - lo)) is within
+// 2^-24*(|v| + |uf|) < 5e-5 of v + zp - lo (v = x/scale in fp64) wherever the
+// result is not clipped (|v| <= 511, |uf| <= 256), so when uf is more than
+// 2.5e-4 away from a half-integer, rint(uf) is the reference's rounding of v
+// (half-away and half-even agree off ties; the 2^-16 snap only moves values
+// onto the integer they round to anyway), and the clip to [0, 255] matches
+// quantizer.py:130.  Near a tie, NaN or +-inf: the exact boundary table.
+__device__ __forceinline__ int quant_near_u(const QuantCtx &q, float x) {
+    const float uf = fmaf(x, q.inv, q.zpo);
+    const float r = rintf(uf);
+    if (fabsf(uf - r) < 0.49975f) return min(max((int)r, 0), 255);
+    if (!q.table) return quantize_one(x, q.scale, q.zp, q.sgn, q.round) - q.lo;  // exact fp64 (NaN -> flagged)
+    return quant_exact(q, x) - q.lo;
+}
+__device__ __forceinline__ int quant_any_u(const QuantCtx &q, float x, bool nearest) {
+    if (nearest) return quant_near_u(q, x);
+    if (!q.table) return quantize_one(x, q.scale, q.zp, q.sgn, q.round) - q.lo;
+    return quant_exact(q, x) - q.lo;
+}
+
 template <int G>
 __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restrict__ x, int64_t n, int64_t h, int64_t w,
                                                            int c, int64_t cs, int pt, int pl, int64_t hp, int64_t wp,
                                                            FastDiv fd_hp, FastDiv fd_wp,
-                                                           const axb_qparams *__restrict__ prm, int is_signed,
-                                                           uint8_t *__restrict__ codes, int32_t *__restrict__ pixsum,
-                                                           int32_t *d_flags) {
+                                                           axb_qparams *prm, const int32_t *d_range, int is_signed,
+                                                           int round_mode, uint8_t *__restrict__ codes,
+                                                           int32_t *__restrict__ pixsum, int32_t *d_flags) {
     __shared__ QuantCtx q;
-    quant_ctx_load(q, prm, is_signed);
+    if (d_range)
+        quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
+    else
+        quant_ctx_load(q, prm, is_signed);
+    const bool nearest = round_mode != AXB_ROUND_TOWARD_ZERO;
     const int lane = threadIdx.x & 31;
     const int64_t npix = n * hp * wp;
     const bool vec = (c % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
     const int zpb = q.zp & 0xFF;
+    const uint32_t zpw = (uint32_t)zpb * 0x01010101u;
     int nonfinite = 0;
-    auto group = [&](int64_t p, int64_t g, int32_t &s) -> uint32_t {
-        // npix < 2^32 (checked on the host): 32-bit magic-number division
-        const uint32_t t = fdiv((uint32_t)p, fd_wp);
-        const int64_t xw = (uint32_t)p - t * (uint32_t)wp;
+    // one 4-channel group g of padded pixel p -> 4 code bytes; s += their code values
+    auto group = [&](uint32_t p, int g, int32_t &s) -> uint32_t {
+        const uint32_t t = fdiv(p, fd_wp);  // npix < 2^31 (checked on the host)
+        const int xw = (int)(p - t * (uint32_t)wp);
         const uint32_t b = fdiv(t, fd_hp);
-        const int64_t yh = t - b * (uint32_t)hp;
-        const int64_t iy = yh - pt, ix = xw - pl;
-        const int c0 = (int)g * 4;
-        uint32_t word = 0;
-        if (iy >= 0 && iy < h && ix >= 0 && ix < w) {
-            const float *src = x + ((b * h + iy) * w + ix) * c + c0;
-            float e[4];
-            if (vec && c0 + 3 < c) {
-                const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
-                e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) e[k] = (c0 + k < c) ? src[k] : 0.0f;
+        const int yh = (int)(t - b * (uint32_t)hp);
+        const int iy = yh - pt, ix = xw - pl;
+        const int c0 = g * 4;
+        if (iy < 0 || iy >= h || ix < 0 || ix >= w) {  // zero-point border (axconv.py:185-189)
+            if (c0 + 3 < c) {
+                s += 4 * q.zp;
+                return zpw;
             }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (c0 + k < c) {
-                    nonfinite |= !isfinite(e[k]);
-                    const int code = quant_exact(q, e[k]);
-                    s += code;
-                    word |= (uint32_t)(code & 0xFF) << (8 * k);
-                }
-            }
-        } else {
+            uint32_t word = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (c0 + k < c) {
                     s += q.zp;
                     word |= (uint32_t)zpb << (8 * k);
                 }
+            return word;
         }
+        const float *src = x + (((int64_t)b * h + iy) * w + ix) * c + c0;
+        float e[4];
+        if (vec && c0 + 3 < c) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
+            e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) e[k] = (c0 + k < c) ? __ldg(src + k) : 0.0f;
+        }
+        uint32_t word = 0;
+        int su = 0, nv = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (c0 + k < c) {
+                nonfinite |= !(fabsf(e[k]) <= 3.402823466e38f);
+                const int u = quant_any_u(q, e[k], nearest);
+                su += u;
+                ++nv;
+                word |= (uint32_t)((u + q.lo) & 0xFF) << (8 * k);
+            }
+        }
+        s += su + nv * q.lo;
         return word;
     };
     if constexpr (G > 0) {
-        const int64_t total = npix * G;
-        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        const int64_t bound = (total + 31) / 32 * 32;
-        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < bound; i += stride) {
+        // thread per 4-channel group (float4 in, u32 out, coalesced); segmented warp sum per pixel
+        const uint32_t total = (uint32_t)(npix * G);
+        const uint32_t stride = gridDim.x * blockDim.x;
+        const uint32_t bound = (total + 31u) & ~31u;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < bound; i += stride) {
             int32_t s = 0;
             if (i < total) {
-                const int64_t p = i / G;
-                const uint32_t word = group(p, i % G, s);
+                const uint32_t word = group(i / G, (int)(i % G), s);
                 reinterpret_cast<uint32_t *>(codes)[i] = word;  // cs == 4G: group i is word i
             }
 #pragma unroll
@@ -183,10 +270,107 @@ __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restri
         for (int64_t p = warp0; p < npix; p += nwarps) {
             int32_t s = 0;
             for (int64_t g = lane; g < cs / 4; g += 32)
-                reinterpret_cast<uint32_t *>(codes + p * cs)[g] = group(p, g, s);
+                reinterpret_cast<uint32_t *>(codes + p * cs)[g] = group((uint32_t)p, (int)g, s);
 #pragma unroll
             for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) pixsum[p] = s;
+        }
+    }
+    range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
+}
+
+// Fast K2 for c % 16 == 0 (no channel padding): one thread per 16-channel chunk
+// (4 x float4 in, one 16-byte code store), C16 = c/16 chunks per pixel.  Per
+// element: FFMA + FRND + tie test + clamp; codes are packed as offsets u and the
+// pixel sum is dp4a(u bytes) + 16*lo per chunk (exact).  Any element the fp32
+// estimate cannot decide (near a half-step, NaN/inf) or a toward-zero table
+// sends its whole chunk through the exact path (rare, warp-divergent).
+template <int C16>
+__global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__restrict__ x, int n, int h, int w,
+                                                             int pt, int pl, int hp, int wp, FastDiv fd_hp,
+                                                             FastDiv fd_wp, axb_qparams *prm,
+                                                             const int32_t *d_range, int is_signed, int round_mode,
+                                                             uint8_t *__restrict__ codes,
+                                                             int32_t *__restrict__ pixsum, int32_t *d_flags) {
+    __shared__ QuantCtx q;
+    if (d_range)
+        quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
+    else
+        quant_ctx_load(q, prm, is_signed);
+    const bool nearest = round_mode != AXB_ROUND_TOWARD_ZERO;
+    const float inv = q.inv, zpo = q.zpo;
+    const int lo = q.lo;
+    const uint32_t flip = is_signed ? 0x80808080u : 0u;  // raw byte of code lo+u = (u + lo) & 0xFF
+    const uint32_t zpw = (uint32_t)(q.zp & 0xFF) * 0x01010101u;
+    const int zsum = 16 * q.zp;
+    const int c = 16 * C16;
+    int nonfinite = 0;
+    const uint32_t npix = (uint32_t)n * (uint32_t)hp * (uint32_t)wp;
+    constexpr int PER = C16 <= 32 ? C16 : 32;  // lanes per pixel in the segmented sum
+    const uint32_t total = npix * (uint32_t)C16;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t bound = (total + 31u) & ~31u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < bound; i += stride) {
+        int32_t s = 0;
+        uint32_t p = 0, j = 0;
+        if (i < total) {
+            p = i / C16;
+            j = i % C16;
+            const uint32_t t = fdiv(p, fd_wp);
+            const int xw = (int)(p - t * (uint32_t)wp);
+            const uint32_t b = fdiv(t, fd_hp);
+            const int yh = (int)(t - b * (uint32_t)hp);
+            const int iy = yh - pt, ix = xw - pl;
+            uint4 out;
+            if (iy < 0 || iy >= h || ix < 0 || ix >= w) {  // zero-point border (axconv.py:185-189)
+                out = make_uint4(zpw, zpw, zpw, zpw);
+                s = zsum;
+            } else {
+                const float4 *src = reinterpret_cast<const float4 *>(
+                    x + (((int64_t)b * h + iy) * w + ix) * c + j * 16);
+                float e[16];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float4 f = __ldg(src + v);
+                    e[4 * v] = f.x; e[4 * v + 1] = f.y; e[4 * v + 2] = f.z; e[4 * v + 3] = f.w;
+                }
+                int u[16];
+                bool ok = nearest;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const float uf = fmaf(e[k], inv, zpo);
+                    const float r = rintf(uf);
+                    ok &= fabsf(uf - r) < 0.49975f;  // false near a tie and for NaN / +-inf
+                    u[k] = min(max((int)r, 0), 255);
+                }
+                if (__builtin_expect(!ok, 0)) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        nonfinite |= !(fabsf(e[k]) <= 3.402823466e38f);
+                        u[k] = quant_any_u(q, e[k], nearest);
+                    }
+                }
+                uint32_t wv[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    wv[v] = (uint32_t)u[4 * v] | ((uint32_t)u[4 * v + 1] << 8) | ((uint32_t)u[4 * v + 2] << 16) |
+                            ((uint32_t)u[4 * v + 3] << 24);
+                uint32_t su = 0;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) su = __dp4a(wv[v], 0x01010101u, su);
+                s = (int32_t)su + 16 * lo;
+                out = make_uint4(wv[0] ^ flip, wv[1] ^ flip, wv[2] ^ flip, wv[3] ^ flip);
+            }
+            reinterpret_cast<uint4 *>(codes)[i] = out;  // chunk i of the padded code tensor
+        }
+        if constexpr (C16 > 1) {
+#pragma unroll
+            for (int o = PER / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        }
+        if constexpr (C16 <= 32) {
+            if (i < total && j == 0) pixsum[p] = s;
+        } else {
+            if (i < total && (j & 31) == 0) atomicAdd(pixsum + p, s);  // pixsum zeroed on the host side
         }
     }
     range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
@@ -367,17 +551,39 @@ int axb_params_upload(const axb_qparams *host_params, axb_qparams *d_params, voi
     return check_launch("params_upload");
 }
 
-int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
-                     int32_t pl, int32_t pr, int64_t cs, const axb_qparams *d_params, int is_signed,
-                     int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags, void *stream) {
+static int quantize_pad_launch(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
+                               int32_t pl, int32_t pr, int64_t cs, axb_qparams *d_params, const int32_t *d_range,
+                               int is_signed, int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags,
+                               void *stream) {
     if (cs != axb_channel_stride(c)) return set_error(AXB_E_VALUE, "channel stride mismatch");
     const int64_t hp = h + pt + pb, wp = w + pl + pr;
     const int64_t total = n * hp * wp;
     if (total == 0) return AXB_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t cap = (int64_t)sm_count() * 16;
-    if (total >= (int64_t(1) << 32)) return set_error(AXB_E_VALUE, "quantize: more than 2^32 padded pixels");
+    // one resident wave (the in-kernel coefficient prologue is paid once per CTA)
+    const int64_t cap = (int64_t)sm_count() * 6;
+    if (total * (cs / 4) >= (int64_t(1) << 31)) return set_error(AXB_E_VALUE, "quantize: more than 2^31 code words");
     const FastDiv fhp = make_fastdiv((uint32_t)hp), fwp = make_fastdiv((uint32_t)wp);
+    const int64_t c16 = c / 16;
+    if (c % 16 == 0 && c16 <= 32 && (c16 & (c16 - 1)) == 0 && ((reinterpret_cast<uintptr_t>(d_x) & 15) == 0)) {
+        int64_t blocks = (total * c16 + 255) / 256;
+        const int64_t cap16 = (int64_t)sm_count() * 8;
+        if (blocks > cap16) blocks = cap16;
+#define AXB_Q16(CC)                                                                                                 \
+    quantize_pad16_kernel<CC><<<(int)blocks, 256, 0, s>>>(d_x, (int)n, (int)h, (int)w, pt, pl, (int)hp, (int)wp,    \
+                                                          fhp, fwp, d_params, d_range, is_signed, round_mode,       \
+                                                          d_codes, d_pixsum, d_flags)
+        switch (c16) {
+            case 1: AXB_Q16(1); break;
+            case 2: AXB_Q16(2); break;
+            case 4: AXB_Q16(4); break;
+            case 8: AXB_Q16(8); break;
+            case 16: AXB_Q16(16); break;
+            default: AXB_Q16(32); break;
+        }
+#undef AXB_Q16
+        return check_launch("quantize_pad16");
+    }
     const int64_t G = cs / 4;
     const int64_t work = (G <= 32 && (G & (G - 1)) == 0) ? total * G : total * 32;
     int64_t blocks = (work + 255) / 256;
@@ -385,7 +591,7 @@ int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t 
     if (blocks < 1) blocks = 1;
 #define AXB_QLAUNCH(GG)                                                                                             \
     quantize_pad_kernel<GG><<<(int)blocks, 256, 0, s>>>(d_x, n, h, w, (int)c, cs, pt, pl, hp, wp, fhp, fwp, d_params, \
-                                                        is_signed, d_codes, d_pixsum, d_flags)
+                                                        d_range, is_signed, round_mode, d_codes, d_pixsum, d_flags)
     switch (G) {
         case 4: AXB_QLAUNCH(4); break;
         case 8: AXB_QLAUNCH(8); break;
@@ -395,6 +601,22 @@ int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t 
     }
 #undef AXB_QLAUNCH
     return check_launch("quantize_pad");
+}
+
+int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
+                     int32_t pl, int32_t pr, int64_t cs, const axb_qparams *d_params, int is_signed,
+                     int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags, void *stream) {
+    return quantize_pad_launch(d_x, n, h, w, c, pt, pb, pl, pr, cs, const_cast<axb_qparams *>(d_params), nullptr,
+                               is_signed, round_mode, d_codes, d_pixsum, d_flags, stream);
+}
+
+int axb_quantize_pad_range(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
+                           int32_t pl, int32_t pr, int64_t cs, const int32_t *d_range, int is_signed, int round_mode,
+                           axb_qparams *d_params_out, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags,
+                           void *stream) {
+    if (!d_range || !d_params_out) return set_error(AXB_E_VALUE, "null range or parameter buffer");
+    return quantize_pad_launch(d_x, n, h, w, c, pt, pb, pl, pr, cs, d_params_out, d_range, is_signed, round_mode,
+                               d_codes, d_pixsum, d_flags, stream);
 }
 
 int64_t axb_filter_kpad(int64_t kh, int64_t kw, int64_t cs) { return (kh * kw * cs + 15) / 16 * 16; }

@@ -7,7 +7,8 @@ synchronisation until the final flag check:
 * ``Min``/``Max`` range nodes (graph.py:270-275) are fused into whoever
   produces the tensor: the conv epilogue, the pool / add kernels, or a
   standalone range kernel (K1) for the graph input.  Ranges stay on device;
-  coefficients are computed on device (``axb_coeffs_from_range``).
+  coefficients are computed on device, in the quantize kernel's prologue
+  (``axb_quantize_pad_range``).
 * ``AxConv2D`` (graph.py:248-269) = K2 quantize/zp-pad + K3 LUT implicit GEMM
   whose epilogue also applies the bias and, when the graph allows it, the
   residual ``Add`` (graph.py:282-286) and ``ReLU`` (graph.py:276-277).

@@ -4,8 +4,8 @@ Filters are quantized once at construction (the reference re-quantizes them
 on every call, axconv.py:287; hoisting is bit-neutral because the filter
 range is a constant, graph.py:129-130).  ``run`` executes, stream-ordered:
 
-  coefficients of the input range (device, no sync)      quantizer.py:98-117
-  K2 quantize + zero-point pad                             quantizer.py:120-131, axconv.py:181-189
+  K2 coefficients of the device input range (kernel         quantizer.py:98-117
+     prologue, no sync) + quantize + zero-point pad        quantizer.py:120-131, axconv.py:181-189
   [im2col of the codes, small-channel layers only]         axconv.py:160-196
   K3 LUT implicit GEMM + fused epilogue                    axconv.py:136-146, :246-256, graph.py:268-286
 
@@ -101,14 +101,17 @@ class ConvLayer:
             return out
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self.launches = 0
-        if in_range_dev is not None:
-            _lib.check(lib.axb_coeffs_from_range(in_range_dev, self.sgn, self.round, self.params[0].data_ptr(), stream))
-            self.launches += 1
         qflag = quant_flag if quant_flag is not None else out_flag
         codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
         pixsum = torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
-        _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, self.params[0].data_ptr(),
-                                        self.sgn, self.round, codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
+        if in_range_dev is not None:  # coefficients of the device range computed inside the quantize kernel
+            _lib.check(lib.axb_quantize_pad_range(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, in_range_dev,
+                                                  self.sgn, self.round, self.params[0].data_ptr(), codes.data_ptr(),
+                                                  pixsum.data_ptr(), qflag, stream))
+        else:
+            _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs,
+                                            self.params[0].data_ptr(), self.sgn, self.round, codes.data_ptr(),
+                                            pixsum.data_ptr(), qflag, stream))
         self.launches += 1
         d = _lib.ConvDesc()
         if self.kp:

@@ -357,3 +357,68 @@ def test_depthwise_matches_per_channel_oracle(stride, shape, mode):
     flags = torch.zeros(2, dtype=torch.int32, device="cuda")
     y = layer.run(torch.from_numpy(x).cuda(), None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr())
     assert bits_equal(y.cpu().numpy(), want)
+
+
+def test_quantizer_fast_path_sweep():
+    """quantize_pad (fp32 estimate + tie fallback) vs quantize_values on dense near-tie sweeps:
+    values within a few ulps of every half-step and every integer step, random ranges, all modes,
+    plus out-of-range values (clipping) -- bit-exact codes and pixel sums."""
+    torch = _torch()
+    from paper_2002_09481_b200 import _lib
+
+    lib = _lib.load()
+    s = torch.cuda.current_stream().cuda_stream
+    rng = np.random.default_rng(77)
+    rounds = {O.HALF_AWAY: 0, O.HALF_EVEN: 1, O.TOWARD_ZERO: 2}
+    for trial in range(24):
+        mode = (O.SIGNED, O.UNSIGNED)[trial % 2]
+        rname = list(rounds)[trial % 3]
+        mn = float(-abs(rng.standard_normal()) * 10 ** rng.uniform(-3, 3)) if trial % 4 else 0.0
+        mx = float(abs(rng.standard_normal()) * 10 ** rng.uniform(-3, 3))
+        scale, zp = O.compute_coeffs(mn, mx, mode, rname)
+        lo, _ = O.bounds(mode)
+        k = np.arange(-300, 300, dtype=np.float64)
+        base = np.concatenate([(k + 0.5 - zp + lo) * scale, (k - zp + lo) * scale]).astype(np.float32)
+        ulps = np.arange(-3, 4, dtype=np.int32)
+        near = (base.view(np.int32)[:, None] + ulps[None, :]).reshape(-1).view(np.float32)
+        vals = np.concatenate([near, rng.uniform(mn * 1.5, mx * 1.5, 50000).astype(np.float32)])
+        vals = vals[np.isfinite(vals)]
+        hp_ = _lib.QParams()
+        _lib.check(lib.axb_coeffs_host(mn, mx, int(mode == O.SIGNED), rounds[rname], hp_))
+        prm = torch.zeros(_lib.QPARAMS_BYTES, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.axb_params_upload(hp_, prm.data_ptr(), s))
+        for c in (4, 16, 64):  # 4: per-word kernel; 16, 64: 16-channel-chunk kernel
+            v = vals[: len(vals) // c * c]
+            want = O.quantize_values(v, scale, zp, mode, rname)
+            n = len(v) // c
+            cs = max(16, c)
+            x = torch.from_numpy(v.reshape(1, 1, n, c)).cuda()
+            codes = torch.empty(n * cs, dtype=torch.uint8, device="cuda")
+            pixsum = torch.empty(n, dtype=torch.int32, device="cuda")
+            fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+            _lib.check(lib.axb_quantize_pad(x.data_ptr(), 1, 1, n, c, 0, 0, 0, 0, cs, prm.data_ptr(),
+                                            int(mode == O.SIGNED), rounds[rname], codes.data_ptr(), pixsum.data_ptr(),
+                                            fl.data_ptr(), s))
+            cb = codes.cpu().numpy().reshape(n, cs)
+            got = cb[:, :c].reshape(-1).view(np.int8 if mode == O.SIGNED else np.uint8)
+            assert np.array_equal(got, want), (trial, c, mode, rname, np.flatnonzero(got != want)[:5])
+            assert (cb[:, c:] == 0).all()
+            assert np.array_equal(pixsum.cpu().numpy(), want.reshape(n, c).astype(np.int32).sum(1)), (trial, c)
+            assert int(fl.item()) == 0
+            # the fused path: coefficients of a device range computed in the kernel prologue
+            mn32, mx32 = np.float32(mn), np.float32(mx)
+            s2, zp2 = O.compute_coeffs(float(mn32), float(mx32), mode, rname)
+            want2 = O.quantize_values(v, s2, zp2, mode, rname)
+            ordv = np.array([mn32, mx32], np.float32).view(np.int32)
+            ordv = np.where(ordv >= 0, ordv, ordv ^ 0x7FFFFFFF).astype(np.int32)
+            rng_d = torch.from_numpy(ordv).cuda()
+            prm2 = torch.zeros(_lib.QPARAMS_BYTES, dtype=torch.uint8, device="cuda")
+            _lib.check(lib.axb_quantize_pad_range(x.data_ptr(), 1, 1, n, c, 0, 0, 0, 0, cs, rng_d.data_ptr(),
+                                                  int(mode == O.SIGNED), rounds[rname], prm2.data_ptr(),
+                                                  codes.data_ptr(), pixsum.data_ptr(), fl.data_ptr(), s))
+            cb = codes.cpu().numpy().reshape(n, cs)
+            got = cb[:, :c].reshape(-1).view(np.int8 if mode == O.SIGNED else np.uint8)
+            assert np.array_equal(got, want2), (trial, c, "range", np.flatnonzero(got != want2)[:5])
+            assert np.array_equal(pixsum.cpu().numpy(), want2.reshape(n, c).astype(np.int32).sum(1))
+            pb = prm2.cpu().numpy()
+            assert pb[:8].view(np.float64)[0] == s2 and pb[8:12].view(np.int32)[0] == zp2
