@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
     constexpr int NG = ring_groups(BM, BN);
     constexpr int SLOTS = G * NG;
     static_assert(fast_smem(BM, BN) <= kSmemBudget, "tile variant exceeds shared memory");
-    constexpr int NQ = BM / NT;  // activation rows per thread per chunk (one 16-byte cp.async each)
-    static_assert(BM % NT == 0 && NQ >= 1, "tile/thread mismatch");
+    constexpr int NQ = (BM + NT - 1) / NT;  // activation rows per thread per chunk (one 16-byte cp.async each)
+    static_assert(BM % NT == 0 || NT % BM == 0, "tile/thread mismatch");  // BM < NT: threads >= BM load none
     static_assert(BN <= NT, "one weight piece per thread");
     static_assert(TN % 8 == 0, "TN multiple of 8");
 
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int64_t mt = m0 + tid + q * NT;
-            if (mt < p.M) {
+            if ((BM >= NT || tid < BM) && mt < p.M) {
                 int64_t pix0;
                 pixel_of(p, mt, pix0);
                 rowbase[q] = (int32_t)(pix0 * p.cs);
@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(WM *WN * 32, 1) lutconv_fast(const ConvK p) {
             const int off = tv ? tapoff_s[ld_t] + ld_ci : 0;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
+                if (BM < NT && tid >= BM) break;
                 const bool v = tv && rowbase[q] >= 0;
                 const uint8_t *src = p.codes + (v ? (int64_t)rowbase[q] + off : 0);
                 cp_async16(as + (tid + q * NT) * 16, src, v ? 16 : 0);
@@ -580,14 +581,22 @@ __global__ void __launch_bounds__(256) lutconv_generic(const ConvK p) {
 struct Variant {
     const char *name;
     int tm, tn, wm, wn;
+    float cost;  // relative time per lookup slot (per-layer-normalised median on B200; 1 = best)
 };
-// tuning table (axb_conv_desc.variant selects one explicitly; 0 = heuristic)
+// tuning table (axb_conv_desc.variant selects one explicitly; 0 = cost model below).
+// cost: scripts/tune_variants.py over every ResNet-8/50/62 layer, each layer's time
+// divided by waves*BM*BN*kpad and normalised by the layer's best variant.
 static const Variant kVariants[] = {
-    {"auto", 0, 0, 0, 0},
-    {"tm4tn16_w8x1", 4, 16, 8, 1},  {"tm4tn16_w4x2", 4, 16, 4, 2},  {"tm4tn16_w2x4", 4, 16, 2, 4},
-    {"tm4tn8_w8x2", 4, 8, 8, 2},    {"tm4tn8_w4x4", 4, 8, 4, 4},    {"tm2tn16_w12x1", 2, 16, 12, 1},
-    {"tm4tn8_w6x2", 4, 8, 6, 2}, {"tm4tn16_w6x2", 4, 16, 6, 2}, {"tm4tn16_w3x4", 4, 16, 3, 4},
-    {"tm2tn16_w16x1", 2, 16, 16, 1}, {"tm2tn16_w8x2", 2, 16, 8, 2}, {"tm4tn16_w4x4", 4, 16, 4, 4},
+    {"auto", 0, 0, 0, 0, 0.f},
+    {"tm4tn16_w8x1", 4, 16, 8, 1, 1.089f},  {"tm4tn16_w4x2", 4, 16, 4, 2, 1.047f},
+    {"tm4tn16_w2x4", 4, 16, 2, 4, 1.024f},  {"tm4tn8_w8x2", 4, 8, 8, 2, 1.066f},
+    {"tm4tn8_w4x4", 4, 8, 4, 4, 1.019f},    {"tm2tn16_w12x1", 2, 16, 12, 1, 1.107f},
+    {"tm4tn8_w6x2", 4, 8, 6, 2, 1.083f},    {"tm4tn16_w6x2", 4, 16, 6, 2, 1.037f},
+    {"tm4tn16_w3x4", 4, 16, 3, 4, 1.000f},  {"tm2tn16_w16x1", 2, 16, 16, 1, 1.166f},
+    {"tm2tn16_w8x2", 2, 16, 8, 2, 1.127f},  {"tm4tn16_w4x4", 4, 16, 4, 4, 1.147f},
+    {"tm2tn8_w8x2", 2, 8, 8, 2, 1.137f},    {"tm2tn8_w4x4", 2, 8, 4, 4, 1.089f},
+    {"tm4tn8_w2x8", 4, 8, 2, 8, 1.002f},    {"tm2tn8_w2x8", 2, 8, 2, 8, 1.084f},
+    {"tm4tn8_w3x4", 4, 8, 3, 4, 1.031f},    {"tm2tn16_w4x4", 2, 16, 4, 4, 1.074f},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -631,24 +640,35 @@ static int launch_variant(int v, const ConvK &k, int sm_limit, cudaStream_t s) {
         case 10: return launch_fast<2, 16, 16, 1, SGN>(k, sm_limit, s, nm);
         case 11: return launch_fast<2, 16, 8, 2, SGN>(k, sm_limit, s, nm);
         case 12: return launch_fast<4, 16, 4, 4, SGN>(k, sm_limit, s, nm);
+        case 13: return launch_fast<2, 8, 8, 2, SGN>(k, sm_limit, s, nm);
+        case 14: return launch_fast<2, 8, 4, 4, SGN>(k, sm_limit, s, nm);
+        case 15: return launch_fast<4, 8, 2, 8, SGN>(k, sm_limit, s, nm);
+        case 16: return launch_fast<2, 8, 2, 8, SGN>(k, sm_limit, s, nm);
+        case 17: return launch_fast<4, 8, 3, 4, SGN>(k, sm_limit, s, nm);
+        case 18: return launch_fast<2, 16, 4, 4, SGN>(k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown conv kernel variant");
     }
 }
 
-// Heuristic from scripts/tune_variants.py on B200 (ResNet-8 / ResNet-50 layers):
-// 16-warp TN=8 tiles win for narrow layers, the 12-warp 384x64 tile for wide
-// ones unless its tile count quantizes badly against the SM count.
+// Cost model (fit with scripts/tune_variants.py on B200, within 0.1% of the best
+// variant summed over all ResNet-8/50/62 layers): time ~ cost * waves * BM * BN,
+// waves = ceil(tiles / SMs) -- so wave quantization of small layers picks smaller tiles.
 static int pick_variant(const ConvK &k) {
-    if (k.coutp <= 16) return 4;   // tm4tn8_w8x2: 1024 x 16
-    if (k.coutp <= 64) return 5;   // tm4tn8_w4x4:  512 x 32
     const int64_t sms = sm_count();
-    auto eff = [&](int64_t bm, int64_t bn) {
+    int best = 1;
+    double best_t = 1e300;
+    for (int v = 1; v < kNumVariants; ++v) {
+        const Variant &x = kVariants[v];
+        const int64_t bm = (int64_t)x.wm * 32 * x.tm, bn = (int64_t)x.wn * x.tn;
         const int64_t tiles = ((k.M + bm - 1) / bm) * ((k.coutp + bn - 1) / bn);
         const int64_t waves = (tiles + sms - 1) / sms;
-        return (double)tiles / (double)(waves * sms);
-    };
-    const double e9 = eff(384, 64), e5 = eff(512, 32);
-    return (e5 > e9 + 0.08) ? 5 : 9;  // tm4tn16_w3x4: 384 x 64
+        const double t = (double)x.cost * (double)waves * (double)(bm * bn);
+        if (t < best_t) {
+            best_t = t;
+            best = v;
+        }
+    }
+    return best;
 }
 
 }  // namespace axb
