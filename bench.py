@@ -280,65 +280,78 @@ def main():
 
     imgs, labels = make_images(spec["kind"], batch, seed=(1000 + rank) if not spec.get("sweep") else 1000)
     x_dev = torch.from_numpy(imgs).to(dev)
-    x_host = torch.from_numpy(imgs).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    # warm-up (also prepares filters once: hoisted quantize_filters)
+    # warm-up (also prepares filters once: hoisted quantize_filters), then CUDA-graph capture
     for _ in range(args.warmup):
         ys = run_all(x_dev, check=True)
     torch.cuda.synchronize()
     launches = sum(g.launches for g in graphs)
+    for g in graphs:
+        g.capture(tuple(x_dev.shape))
+    for _ in range(args.warmup):
+        ys = [g.replay(x_dev) for g in graphs]
+    torch.cuda.synchronize()
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ------------------------------------------------ device-resident timed region
+    # ------------------------------------------------ device-resident timed region (graph replay)
     sampler = ClockSampler(local)
     sampler.start()
-    profile: list = []
     barrier()
     step_ms = []
     for _ in range(args.steps):
         flush.zero_()  # write > L2 (126 MB) between timed steps
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        ys = run_all(x_dev, profile=profile)
+        ys = [g.replay(x_dev, check=False) for g in graphs]
         e1.record()
         step_ms.append((e0, e1))
     barrier()
     clocks = sampler.stop()
     per_step = [a.elapsed_time(b) for a, b in step_ms]
     total_ms = sum(per_step)
-    conv_ms = sum(a.elapsed_time(b) for _, a, b, _ in profile)
-    conv_macs = sum(m for *_, m in profile)
-    layer_rows = {}
-    for nid, a, b, m in profile:
-        r = layer_rows.setdefault(nid, [0.0, 0, 0])
-        r[0] += a.elapsed_time(b)
-        r[1] += m
-        r[2] += 1
     for g in graphs:
         g.check_flags()
     y = torch.stack([t.reshape(batch, -1) for t in ys])  # (nets, batch, classes)
 
-    # ------------------------------------------------ end-to-end through the public API (host buffers)
-    out_host = torch.empty(tuple(y.shape), dtype=torch.float32).pin_memory()
+    # ------------------------------------------------ LUT-conv kernel times (eager pass, events per launch)
+    profile: list = []
     barrier()
-    e2e_ms = []
     for _ in range(args.steps):
         flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        xd = x_host.to(dev, non_blocking=True)
-        yd = torch.stack([t.reshape(batch, -1) for t in run_all(xd)])
-        out_host.copy_(yd, non_blocking=True)
-        e1.record()
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
+        run_all(x_dev, profile=profile)
     barrier()
-    e2e_total = sum(e2e_ms)
+    conv_ms = sum(a.elapsed_time(b) for _, a, b, _, _ in profile) / args.steps
+    conv_macs = sum(m for _, _, _, m, _ in profile) / args.steps
+    conv_algo_bytes = sum(ab for *_, ab in profile) / args.steps
+    conv_launches = len(profile) // args.steps
+    layer_rows = {}
+    for nid, a, b, m, _ in profile:
+        r = layer_rows.setdefault(nid, [0.0, 0, 0])
+        r[0] += a.elapsed_time(b)
+        r[1] += m
+        r[2] += 1
+
+    # ------------------------------------------------ end-to-end through the public API (host buffers)
+    # GpuGraph.run_pipelined: pinned host batch -> H2D (copy stream, overlapping the previous
+    # step's compute) -> captured step -> D2H of the logits (+ flags); L2 flushed before each step.
+    x_hosts = [torch.from_numpy(imgs).pin_memory() for _ in range(args.steps)]
+    outs = [[torch.empty(tuple(g._slots[0]["y"].shape), dtype=torch.float32).pin_memory()
+             for _ in range(args.steps)] for g in graphs]
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for g, o in zip(graphs, outs):
+        g.run_pipelined(x_hosts, o, before_step=flush.zero_)
+    e1.record()
+    barrier()
+    e2e_total = e0.elapsed_time(e1)
+    for o, t in zip(outs, ys):  # the host logits of the last e2e step == the device-timed run's
+        assert torch.equal(o[-1].view(torch.int32), t.cpu().view(torch.int32))
 
     # ------------------------------------------------ max over ranks, NCCL gather of logits/counts
     from paper_2002_09481_b200.dist import exchange_results
@@ -370,13 +383,23 @@ def main():
     peak_lookups = sm_count * 32 * max_mhz * 1e6  # one 32-lane LDS wavefront per SM per clock
     achieved = conv_macs / (conv_ms / 1e3) if conv_ms else 0.0
     sampled = clocks.get("sm_mhz")
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{args.workload}.json"
+    if tf.exists():
+        try:
+            traffic = _json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
     roofline = {
         "bound": "smem", "kernel": "lutconv_fast (LUT implicit GEMM, all conv launches of a step)",
         "achieved": round(achieved / 1e9, 2), "peak": round(peak_lookups / 1e9, 2), "unit": "Glookup/s",
         "frac": round(achieved / peak_lookups, 4),
         "frac_at_sampled_clock": round(achieved / (sm_count * 32 * sampled * 1e6), 4) if sampled else None,
         "peak_basis": f"derived: {sm_count} SMs x 32 lookups/clk x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-        "traffic": None, "conv_share_of_step": round(conv_ms / total_ms, 4) if total_ms else None,
+        "traffic": traffic, "traffic_unit": "DRAM bytes per LUT-conv launch (ncu --set full, committed profile)",
+        "algorithmic_bytes_per_launch": int(conv_algo_bytes / max(conv_launches, 1)),
+        "conv_launches_per_step": conv_launches,
+        "conv_share_of_step": round(conv_ms / (total_ms / args.steps), 4) if total_ms else None,
     }
     line = {
         "metric": METRIC, "value": round(gmacs, 2), "unit": "GMAC/s",
@@ -390,10 +413,14 @@ def main():
                    "networks_per_gpu": nets, "macs_per_image": macs_img,
                    "parallelism": (f"dp{world} (candidate tables sharded round-robin)" if spec.get("sweep")
                                    else f"dp{world} (one range-batch per GPU)"),
-                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "step": "one CUDA-graph replay of the whole graph (captured after warm-up)"},
         "roofline": roofline,
         "e2e": {"value": round(e2e_gmacs, 2), "unit": "GMAC/s", "images_per_s": round(images / (e2e_total / 1e3), 2),
-                "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4)},
+                "h2d_bytes_per_step": int(x_hosts[0].numel() * 4 * nets),
+                "d2h_bytes_per_step": int(sum(o[0].numel() * 4 + g.flags.numel() * 4 for g, o in zip(graphs, outs))),
+                "path": "GpuGraph.run_pipelined: pinned host batch, H2D on a copy stream overlapping the previous "
+                        "step, CUDA-graph step, D2H of logits + flags; L2 flushed before every step inside the region"},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
         "agreement_with_labels": round(float(cnt[:-1].sum()) / float(cnt[-1]), 4),

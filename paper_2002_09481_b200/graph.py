@@ -332,7 +332,83 @@ class GpuGraph:
         return out
 
     def check_flags(self):
-        fl = self.flags.cpu().numpy()
+        self._check_flag_array(self.flags.cpu().numpy())
+
+    # ------------------------------------------------------------------ CUDA graphs + pipelined host I/O
+    def capture(self, in_shape, slots: int = 2) -> None:
+        """Record ``run`` for a fixed input shape into ``slots`` CUDA graphs (one per static
+        input buffer).  Replays launch the whole step (range, quantize, LUT convs, pools, ...)
+        with one CPU call; each slot owns its input buffer, output and flag snapshot, so a
+        host->device copy into one slot overlaps compute on another (``run_pipelined``)."""
+        in_shape = tuple(int(v) for v in in_shape)
+        stream = torch.cuda.current_stream(self.device)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(stream)
+        self._slots = []
+        with torch.cuda.stream(side):
+            for _ in range(slots):
+                x = torch.zeros(in_shape, dtype=torch.float32, device=self.device)
+                self.run(x, check=False)  # warm-up: filter prep, shared-memory attributes, allocator
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    y = self.run(x, check=False)
+                    fl = self.flags.clone()
+                self._slots.append({"graph": g, "x": x, "y": y, "flags": fl})
+        stream.wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        self._captured_shape = in_shape
+
+    def replay(self, batch: torch.Tensor, slot: int = 0, check: bool = True) -> torch.Tensor:
+        """One step through the captured graph of ``slot`` (batch copied into its static input)."""
+        sl = self._slots[slot]
+        sl["x"].copy_(batch, non_blocking=True)
+        sl["graph"].replay()
+        if check:
+            self._check_flag_array(sl["flags"].cpu().numpy())
+        return sl["y"]
+
+    def run_pipelined(self, host_batches, host_outputs=None, before_step=None):
+        """End-to-end over pinned HOST batches: H2D of step i+1 (copy stream) overlaps the
+        captured compute of step i; each step's logits and flags come back D2H.  Returns the
+        list of host outputs; raises like ``run`` if any step saw non-finite values."""
+        if not getattr(self, "_slots", None):
+            self.capture(host_batches[0].shape)
+        nsl = len(self._slots)
+        comp = torch.cuda.current_stream(self.device)
+        copy = torch.cuda.Stream(self.device)
+        outs = host_outputs if host_outputs is not None else [
+            torch.empty(tuple(self._slots[0]["y"].shape), dtype=torch.float32).pin_memory() for _ in host_batches]
+        fl_host = torch.empty((len(host_batches), self.flags.numel()), dtype=torch.int32).pin_memory()
+        h2d_done = [torch.cuda.Event() for _ in range(nsl)]
+        slot_free = [torch.cuda.Event() for _ in range(nsl)]
+        for e in slot_free:
+            e.record(comp)
+
+        def h2d(i):
+            sl = self._slots[i % nsl]
+            copy.wait_event(slot_free[i % nsl])  # previous user of the slot has consumed its input
+            with torch.cuda.stream(copy):
+                sl["x"].copy_(host_batches[i], non_blocking=True)
+            h2d_done[i % nsl].record(copy)
+
+        h2d(0)
+        for i in range(len(host_batches)):
+            sl = self._slots[i % nsl]
+            comp.wait_event(h2d_done[i % nsl])
+            if i + 1 < len(host_batches):
+                h2d(i + 1)
+            if before_step is not None:
+                before_step()  # e.g. the benchmark's L2 flush, on the compute stream
+            sl["graph"].replay()
+            outs[i].copy_(sl["y"], non_blocking=True)
+            fl_host[i].copy_(sl["flags"], non_blocking=True)
+            slot_free[i % nsl].record(comp)
+        comp.synchronize()
+        for i in range(len(host_batches)):
+            self._check_flag_array(fl_host[i].numpy())
+        return outs
+
+    def _check_flag_array(self, fl):
         for n in self.nodes:
             if n["kind"] in ("Min", "Max"):
                 tid = self.t(n["inputs"][0])

@@ -157,5 +157,9 @@ class ConvLayer:
         self.launches += 1
         if profile is not None:
             e1.record()
-            profile.append((e0, e1, n * oh * ow * self.kh * self.kw * c * self.cout))
+            # algorithmic HBM bytes of the conv launch: codes (+ per-pixel sums), filter codes,
+            # fp32 output, residual read
+            algo = d.n * d.hp * d.wp * (d.cs + 4) + self.kpad * self.coutp + n * oh * ow * self.cout * (
+                8 if residual is not None else 4)
+            profile.append((e0, e1, n * oh * ow * self.kh * self.kw * c * self.cout, algo))
         return out
