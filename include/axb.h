@@ -144,9 +144,29 @@ typedef struct axb_conv_desc {
     int32_t sm_limit;       /* 0 = all SMs; else cap persistent grid                 */
     int32_t variant;        /* fast-kernel tile variant, 0 = heuristic (tuning)      */
     int32_t pixel_order;    /* lanes -> pixels: 0 auto, 1 row runs, 4 4x8 blocks     */
+    const uint32_t *ftable; /* nullable: filter-specialised product table from
+                               axb_ftable_prepare; when set (and variant == 0) the
+                               packed-pair ftable kernel runs instead of the LUT one */
+    int32_t ft_variant;     /* ftable-kernel tile variant, 0 = cost model            */
+    int32_t reserved0;
 } axb_conv_desc;
 
 int axb_conv2d_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);
+
+/* ---- filter-specialised product table (once per layer and truth table) -----
+ * The filter codes of a layer are constants (graph.py:129-130), so the 256
+ * possible products of every filter code are gathered once:
+ *   W[nb][k][pair][a] = u(lut[(a<<8)|F[k][nb*16+2*pair]]) | u(lut[(a<<8)|F[k][nb*16+2*pair+1]]) << 16
+ * (u = raw ^ 0x8000 for signed tables, raw for unsigned; junk rows = zero
+ * contribution), uint32, axb_ftable_bytes(kpad, coutp) = kpad * coutp * 512 bytes.
+ * kh, kw, c, cs are the filter geometry the conv sees (as axb_filters_prepare).
+ * Replaces no reference function: it is a re-layout of the MultLut (axmult.py:22-43)
+ * restricted to the layer's filter codes (axconv.py:199-210), bit-identical sums. */
+int64_t axb_ftable_bytes(int64_t kpad, int64_t coutp);
+int axb_ftable_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                       const axb_lut *lut, uint32_t *d_ftable, void *stream);
+int axb_ft_variant_count(void);
+const char *axb_ft_variant_name(int variant);
 int axb_conv_variant_count(void);
 /* Depthwise approximate conv (config 5; the reference has no groups): channel c
  * of the output == axconv2d on input channel c alone with the shared ranges.

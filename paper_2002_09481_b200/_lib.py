@@ -56,6 +56,7 @@ class ConvDesc(ctypes.Structure):
         ("bias", c_vp), ("residual", c_vp), ("out", c_vp), ("acc_out", c_vp),
         ("out_range", c_vp), ("flags", c_vp),
         ("force_generic", c_i32), ("sm_limit", c_i32), ("variant", c_i32), ("pixel_order", c_i32),
+        ("ftable", c_vp), ("ft_variant", c_i32), ("reserved0", c_i32),
     ]
 
 
@@ -86,6 +87,10 @@ SIGNATURES = {
                                     c_vp, c_vp, c_vp]),
     "axb_conv2d_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
     "axb_conv_variant_count": (c_int, []),
+    "axb_ftable_bytes": (c_i64, [c_i64, c_i64]),
+    "axb_ftable_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "axb_ft_variant_count": (c_int, []),
+    "axb_ft_variant_name": (ctypes.c_char_p, [c_int]),
     "axb_depthwise_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
     "axb_conv_variant_name": (ctypes.c_char_p, [c_int]),
     "axb_conv_im2col_kp": (c_i64, [c_i64, c_i64, c_i64]),

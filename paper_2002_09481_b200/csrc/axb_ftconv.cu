@@ -1,0 +1,444 @@
+// K3 (ftable path): approximate convolution over a FILTER-SPECIALISED product
+// table, with the same fused epilogue as lutconv_fast.
+//
+// Same arithmetic as axconv.py:136-146 (A[r,c] = sum_k lut[(P[r,k]<<8)|F[c,k]]),
+// :246-256 (corrections, fp64 dequant) and graph.py:268-286 (bias/Add/ReLU); only
+// WHERE the 16-bit products are looked up changes.
+//
+// The filter codes of a layer are constant (graph.py:129-130), so for every
+// filter row k and output-channel pair (c, c+1) the 256 possible products
+//     W[k][pair][a] = ( lut[(a<<8)|F[k][c]] , lut[(a<<8)|F[k][c+1]] )
+// can be gathered ONCE per layer (axb_ftable_prepare) into 32-bit words.  The
+// conv then does, per lane (one output pixel, activation code a at row k):
+//     w = W[k][pair][a]   (one LDS.32 = TWO exact table lookups)
+// i.e. the 16-bit entries are still gathered from shared memory by the
+// activation code, but two channels share one 4-byte bank word, so a 32-lane
+// wavefront delivers up to 64 lookups instead of 32 (LDS.16 on the b-major
+// LUT), and the address of every pair is an immediate offset from one
+// per-(pixel, row) register (no per-lookup IMAD).
+//
+// Exact accumulation of packed pairs: entries are biased to unsigned 16-bit
+// (signed: u = raw ^ 0x8000 = v + 32768), per pair the kernel keeps
+//     all = sum w  (mod 2^32)      hi = sum (w >> 16)   (exact, < 2^32)
+// so  sum u_lo = all - (hi << 16)  (mod 2^32, exact since kpad <= 32768),
+// A = sum u - kpad * 32768 (signed) -- bit-identical int sums.  Junk rows
+// (channel / K padding) hold the zero contribution (u = bias) for every a.
+//
+// Layout in HBM (uint32): [nb = coutp/16][k = 0..kpad-1][pair = 0..7][a = 0..255],
+// i.e. 8 KiB per (channel block, row).  A pipeline stage is KS consecutive rows
+// of one channel block (KS * 8 KiB, contiguous) moved by ONE TMA bulk copy
+// (cp.async.bulk + mbarrier complete_tx) into a ring of ST stages; consumers
+// release a stage with one mbarrier arrive per warp.  Activation codes are read
+// straight from the zp-padded NHWC code tensor into registers (one LDG.128 =
+// 16 rows of one pixel), one 16-row chunk ahead.
+//
+// Tiles: BM = WARPS*32*TM output pixels x 16 channels; tile = nb * ntm + mt, so
+// the CTAs running concurrently share one channel block's table rows in L2.
+#include "axb_convk.cuh"
+
+namespace axb {
+
+constexpr int kFtSubPairs = 4;                     // channel pairs per 8-channel sub-block
+constexpr int kFtRowWords = kFtSubPairs * 256;     // one (sub-block, row) slice: 4 pairs x 256 codes
+constexpr int kFtRowBytes = kFtRowWords * 4;       // 4 KiB
+
+// NPB = channel pairs per tile (4: 8 channels, 8: 16 channels); a stage holds KS rows
+__host__ __device__ constexpr int ft_stage_bytes(int NPB, int KS) { return (NPB / 4) * KS * kFtRowBytes; }
+__host__ __device__ constexpr int ft_smem(int NPB, int KS, int ST) {
+    return ST * ft_stage_bytes(NPB, KS) + kMaxTaps * 4 + 2 * ST * 8;
+}
+
+template <int TM, int WARPS, int NPB, int KS, int ST, bool SGN>
+__global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
+    constexpr int NT = WARPS * 32;
+    constexpr int BM = NT * TM;
+    constexpr int BN = 2 * NPB;
+    constexpr int NSUB = NPB / 4;  // 8-channel sub-blocks per tile
+    constexpr int SPC = 16 / KS;   // pipeline stages per 16-row chunk
+    constexpr uint32_t STAGE_BYTES = ft_stage_bytes(NPB, KS);
+    static_assert(NPB == 4 || NPB == 8, "4 or 8 channel pairs per tile");
+    static_assert(KS == 4 || KS == 8 || KS == 16, "KS rows per stage: 4, 8 or 16");
+    static_assert(ft_smem(NPB, KS, ST) + 512 <= 232448, "ftable ring exceeds shared memory");
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    int32_t *tapoff_s = reinterpret_cast<int32_t *>(smem + ST * STAGE_BYTES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(tapoff_s + kMaxTaps);
+    uint64_t *empty = full + ST;
+    const uint32_t *tab = reinterpret_cast<const uint32_t *>(smem);
+
+    const int tid = (int)threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, WARPS);
+        }
+    }
+    for (int t = tid; t < p.taps; t += NT) tapoff_s[t] = ((t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw) * p.cs;
+    __syncthreads();
+
+    const int64_t grid = gridDim.x;
+    const int64_t my_tiles = p.ntiles > (int64_t)blockIdx.x ? (p.ntiles - blockIdx.x + grid - 1) / grid : 0;
+    const int64_t spt = (int64_t)p.nchunks * SPC;  // stages per tile
+    const int64_t total = my_tiles * spt;
+
+    // ---- producer (thread 0): stage h -> rows [q*KS, q*KS+KS) of tile pr_tile's channel block
+    int64_t pr_h = 0, pr_q = 0, pr_tile = blockIdx.x;
+    auto produce = [&]() {
+        const int slot = (int)(pr_h % ST);
+        const int64_t nb = pr_tile / p.ntm;  // channel block of BN channels = NSUB sub-blocks
+        mbar_expect_tx(full + slot, STAGE_BYTES);
+#pragma unroll
+        for (int sb = 0; sb < NSUB; ++sb) {
+            const uint32_t *src = p.ftable + ((nb * NSUB + sb) * p.kpad + pr_q * KS) * kFtRowWords;
+            bulk_g2s(smem + slot * STAGE_BYTES + sb * (KS * kFtRowBytes), src, KS * kFtRowBytes, full + slot);
+        }
+        ++pr_h;
+        if (++pr_q == spt) {
+            pr_q = 0;
+            pr_tile += grid;
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < ST - 1 && pr_h < total; ++s) produce();
+
+    // ---- activation rows of this lane's TM pixels (int32 offsets: < 2 GiB per launch)
+    int32_t rowbase[TM];
+    auto set_rows = [&](int64_t tile) {
+        const int64_t m0 = (tile % p.ntm) * BM;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int64_t mt = m0 + warp * 32 * TM + i * 32 + lane;
+            int64_t pix0 = 0;
+            if (mt < p.M) pixel_of(p, mt, pix0);
+            rowbase[i] = (int32_t)(pix0 * p.cs);
+        }
+    };
+    uint4 av[TM];
+    int ld_t = 0, ld_ci = 0;  // tap and channel offset of the next chunk to load
+    auto load_chunk = [&]() {
+        const int off = tapoff_s[ld_t] + ld_ci;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) av[i] = __ldg(reinterpret_cast<const uint4 *>(p.codes + rowbase[i] + off));
+        ld_ci += 16;
+        if (ld_ci == p.cs) {
+            ld_ci = 0;
+            ++ld_t;
+        }
+    };
+
+    uint32_t acc_all[TM][NPB], acc_hi[TM][NPB];
+    int32_t spa[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        spa[i] = 0;
+#pragma unroll
+        for (int j = 0; j < NPB; ++j) acc_all[i][j] = acc_hi[i][j] = 0;
+    }
+
+    float tmin = INFINITY, tmax = -INFINITY;
+    int nonfinite = 0;
+    const int64_t bias_units = SGN ? (int64_t)32768 * p.kpad : 0;
+
+    int64_t g = 0;  // consumer stage counter
+    int64_t c_tile = blockIdx.x;
+    if (my_tiles > 0) {
+        set_rows(c_tile);
+        load_chunk();
+    }
+    for (int64_t jt = 0; jt < my_tiles; ++jt) {
+#pragma unroll 1
+        for (int kc = 0; kc < p.nchunks; ++kc) {
+            uint4 cur[TM];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) cur[i] = av[i];
+            if (kc + 1 < p.nchunks) {
+                load_chunk();
+            } else if (jt + 1 < my_tiles) {  // first chunk of the next tile, during this tile's last chunk
+                ld_t = ld_ci = 0;
+                set_rows(c_tile + grid);
+                load_chunk();
+            }
+            // S_p += the 16 code values (junk codes are raw 0 -> value 0), axconv.py:193
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                if (SGN) {
+                    int s = __dp4a((int)cur[i].x, 0x01010101, spa[i]);
+                    s = __dp4a((int)cur[i].y, 0x01010101, s);
+                    s = __dp4a((int)cur[i].z, 0x01010101, s);
+                    spa[i] = __dp4a((int)cur[i].w, 0x01010101, s);
+                } else {
+                    uint32_t s = __dp4a(cur[i].x, 0x01010101u, (uint32_t)spa[i]);
+                    s = __dp4a(cur[i].y, 0x01010101u, s);
+                    s = __dp4a(cur[i].z, 0x01010101u, s);
+                    spa[i] = (int32_t)__dp4a(cur[i].w, 0x01010101u, s);
+                }
+            }
+#pragma unroll 1
+            for (int st = 0; st < SPC; ++st) {
+                const int slot = (int)(g % ST);
+                if (tid == 0 && pr_h < total) {
+                    // refill the slot stage g-1 used, once every warp has released it
+                    if (g >= 1) mbar_wait(empty + (g - 1) % ST, (uint32_t)(((g - 1) / ST) & 1));
+                    produce();
+                }
+                mbar_wait(full + slot, (uint32_t)((g / ST) & 1));
+                const uint32_t *stab = tab + slot * (STAGE_BYTES / 4);
+#pragma unroll
+                for (int kl = 0; kl < KS; ++kl) {
+                    uint32_t ix[TM];  // word index of row kl, code a: kl*1024 + a (sub-block 0)
+#pragma unroll
+                    for (int i = 0; i < TM; ++i) {
+                        const uint32_t wv = kl < 4 ? cur[i].x : (kl < 8 ? cur[i].y : (kl < 12 ? cur[i].z : cur[i].w));
+                        ix[i] = __byte_perm(wv, 0, 0x4440u + (kl & 3)) + kl * kFtRowWords;
+                    }
+#pragma unroll
+                    for (int j = 0; j < NPB; ++j) {
+#pragma unroll
+                        for (int i = 0; i < TM; ++i) {
+                            const uint32_t w = stab[ix[i] + (j / 4) * (KS * kFtRowWords) + (j % 4) * 256];
+                            acc_all[i][j] += w;
+                            acc_hi[i][j] += w >> 16;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + slot);
+#pragma unroll
+                for (int i = 0; i < TM; ++i) {  // next stage's rows move to the front
+                    if (KS == 4) {
+                        cur[i].x = cur[i].y; cur[i].y = cur[i].z; cur[i].z = cur[i].w;
+                    } else if (KS == 8) {
+                        cur[i].x = cur[i].z; cur[i].y = cur[i].w;
+                    }
+                }
+                ++g;
+            }
+        }
+
+        // ------------------------------------------------ fused epilogue for tile c_tile
+        // kpad <= 32768 here, so |A| < 2^31: WRAP32 / SATURATE32 are the identity (axconv.py:128-133)
+        {
+            const EpiConst e = epi_const(p);
+            const int64_t nb = c_tile / p.ntm;
+            const int64_t m0 = (c_tile % p.ntm) * BM;
+            const int cb = (int)nb * BN;
+            const bool full_blk = cb + BN <= p.cout && (p.cout & 3) == 0;
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                const int64_t mt = m0 + warp * 32 * TM + i * 32 + lane;
+                if (mt < p.M) {
+                    int64_t pix0;
+                    const int64_t m = pixel_of(p, mt, pix0);
+                    const int64_t pz = -e.zp2 * (int64_t)spa[i];
+                    float *dst = p.out + m * p.cout + cb;
+                    // four channels (two packed pairs) at a time: float4 stores, few live registers
+#pragma unroll
+                    for (int q = 0; q < NPB / 2; ++q) {
+                        int64_t A[4];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t hi = acc_hi[i][2 * q + h];
+                            const uint32_t lo = acc_all[i][2 * q + h] - (hi << 16);
+                            A[2 * h] = (int64_t)lo - bias_units;
+                            A[2 * h + 1] = (int64_t)hi - bias_units;
+                        }
+                        const int c0 = cb + 4 * q;
+                        if (full_blk) {
+                            float y[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254); fp64 dequant (:256)
+                                const int64_t corr = A[j] + pz - e.zp1 * __ldg(p.fsum + c0 + j) + e.kzz;
+                                y[j] = __double2float_rn(e.scale * __ll2double_rn(corr));
+                                if (p.bias) y[j] = __fadd_rn(y[j], __ldg(p.bias + c0 + j));  // graph.py:268-269
+                            }
+                            if (p.residual) {  // graph.py:282-286
+                                const float4 r = __ldg(reinterpret_cast<const float4 *>(p.residual + m * p.cout + c0));
+                                y[0] = __fadd_rn(y[0], r.x); y[1] = __fadd_rn(y[1], r.y);
+                                y[2] = __fadd_rn(y[2], r.z); y[3] = __fadd_rn(y[3], r.w);
+                            }
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if (p.relu) y[j] = (y[j] > 0.0f || y[j] != y[j]) ? y[j] : 0.0f;  // np.maximum(x, 0)
+                                track(y[j], tmin, tmax, nonfinite);
+                            }
+                            *reinterpret_cast<float4 *>(dst + 4 * q) = make_float4(y[0], y[1], y[2], y[3]);
+                            if (p.acc_out) {
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) p.acc_out[m * p.cout + c0 + j] = A[j];
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if (c0 + j < p.cout) {
+                                    const int64_t corr = A[j] + pz - e.zp1 * p.fsum[c0 + j] + e.kzz;
+                                    float v = __double2float_rn(e.scale * __ll2double_rn(corr));
+                                    if (p.bias) v = __fadd_rn(v, p.bias[c0 + j]);
+                                    if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + c0 + j]);
+                                    if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;
+                                    track(v, tmin, tmax, nonfinite);
+                                    dst[4 * q + j] = v;
+                                    if (p.acc_out) p.acc_out[m * p.cout + c0 + j] = A[j];
+                                }
+                            }
+                        }
+                    }
+                }
+                spa[i] = 0;
+#pragma unroll
+                for (int j = 0; j < NPB; ++j) acc_all[i][j] = acc_hi[i][j] = 0;
+            }
+        }
+        c_tile += grid;
+    }
+    const bool any = tmin <= tmax;
+    range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
+                 AXB_FLAG_OUT_NONFINITE);
+}
+
+// ---------------------------------------------------------------- table preparation
+// W[sb][k][pair][a] = (u(lut[(a<<8)|F[k][c]]), u(lut[(a<<8)|F[k][c+1]])), c = sb*8 + 2*pair (8-channel
+// sub-blocks); u = raw ^ 0x8000 (signed) / raw (unsigned); junk rows (ci >= c or k >= taps*cs) = zero
+// contribution.
+__global__ void ftable_kernel(const uint8_t *__restrict__ fcodes, int64_t kpad, int64_t coutp, int32_t cs, int32_t c,
+                              int64_t kreal, const uint16_t *__restrict__ lut_b, int sgn, uint32_t *__restrict__ out) {
+    const int64_t total = (coutp / 8) * kpad * kFtRowWords;
+    const uint32_t flip = sgn ? 0x8000u : 0u;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = (uint32_t)(idx & 255);
+        const int pr = (int)((idx >> 8) & 3);
+        const int64_t rest = idx >> 10;
+        const int64_t k = rest % kpad;
+        const int64_t sb = rest / kpad;
+        uint32_t w = flip | (flip << 16);  // zero contribution
+        if (k < kreal && (int)(k % cs) < c) {
+            const int64_t col = sb * 8 + 2 * pr;
+            const uint32_t b0 = fcodes[k * coutp + col], b1 = fcodes[k * coutp + col + 1];
+            const uint32_t u0 = (uint32_t)__ldg(lut_b + b0 * 256 + a) ^ flip;
+            const uint32_t u1 = (uint32_t)__ldg(lut_b + b1 * 256 + a) ^ flip;
+            w = u0 | (u1 << 16);
+        }
+        out[idx] = w;
+    }
+}
+
+// ---------------------------------------------------------------- host launch
+struct FtVariant {
+    const char *name;
+    int tm, warps, npb;
+    float cost;  // relative time per lookup slot (1 = best); tuned on B200
+};
+static const FtVariant kFtVariants[] = {
+    {"auto", 0, 0, 0, 0.f},
+    {"ft16_tm2_w16", 2, 16, 8, 1.00f},
+    {"ft16_tm4_w8", 4, 8, 8, 1.06f},
+    {"ft16_tm1_w16", 1, 16, 8, 1.20f},
+    {"ft8_tm4_w16", 4, 16, 4, 1.00f},
+    {"ft8_tm2_w16", 2, 16, 4, 1.05f},
+    {"ft8_tm4_w8", 4, 8, 4, 1.06f},
+    {"ft8_tm4_w16_k8", 4, 16, 4, 1.00f},
+    {"ft8_tm4_w16_k16", 4, 16, 4, 1.00f},
+};
+constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
+
+template <int TM, int WARPS, int NPB, bool SGN, int KS = 4, int ST = 6>
+static int launch_ft(const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
+    constexpr int BM = WARPS * 32 * TM;
+    constexpr int BN = 2 * NPB;
+    const size_t smem = ft_smem(NPB, KS, ST);
+    auto fn = lutconv_ft<TM, WARPS, NPB, KS, ST, SGN>;
+    static int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_ft");
+        configured_dev = dev;
+    }
+    ConvK kk = k;
+    kk.ntm = (int32_t)((k.M + BM - 1) / BM);
+    kk.ntiles = (int64_t)kk.ntm * (k.coutp / BN);
+    int64_t grid = sm_limit > 0 ? sm_limit : sm_count();
+    if (grid > kk.ntiles) grid = kk.ntiles;
+    if (grid < 1) grid = 1;
+    fn<<<(int)grid, WARPS * 32, smem, s>>>(kk);
+    set_last_kernel(name);
+    return check_launch("lutconv_ft");
+}
+
+template <bool SGN>
+static int launch_ft_variant(int v, const ConvK &k, int sm_limit, cudaStream_t s) {
+    const char *nm = kFtVariants[v].name;
+    switch (v) {
+        case 1: return launch_ft<2, 16, 8, SGN>(k, sm_limit, s, nm);
+        case 2: return launch_ft<4, 8, 8, SGN>(k, sm_limit, s, nm);
+        case 3: return launch_ft<1, 16, 8, SGN>(k, sm_limit, s, nm);
+        case 4: return launch_ft<4, 16, 4, SGN>(k, sm_limit, s, nm);
+        case 5: return launch_ft<2, 16, 4, SGN>(k, sm_limit, s, nm);
+        case 6: return launch_ft<4, 8, 4, SGN>(k, sm_limit, s, nm);
+        case 7: return launch_ft<4, 16, 4, SGN, 8, 6>(k, sm_limit, s, nm);
+        case 8: return launch_ft<4, 16, 4, SGN, 16, 3>(k, sm_limit, s, nm);
+        default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
+    }
+}
+
+static int pick_ft_variant(const ConvK &k) {
+    const int64_t sms = sm_count();
+    int best = 1;
+    double best_t = 1e300;
+    for (int v = 1; v < kNumFtVariants; ++v) {
+        const FtVariant &x = kFtVariants[v];
+        const int64_t bm = (int64_t)x.warps * 32 * x.tm, bn = 2 * x.npb;
+        const int64_t tiles = ((k.M + bm - 1) / bm) * (k.coutp / bn);
+        const int64_t waves = (tiles + sms - 1) / sms;
+        const double t = (double)x.cost * (double)waves * (double)(bm * bn);
+        if (t < best_t) {
+            best_t = t;
+            best = v;
+        }
+    }
+    return best;
+}
+
+int conv_ft_launch(const ConvK &k, int variant, int is_signed, int sm_limit, cudaStream_t s) {
+    int v = variant;
+    if (v < 0 || v >= kNumFtVariants) return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
+    if (v == 0) v = pick_ft_variant(k);
+    return is_signed ? launch_ft_variant<true>(v, k, sm_limit, s) : launch_ft_variant<false>(v, k, sm_limit, s);
+}
+
+}  // namespace axb
+
+using namespace axb;
+
+extern "C" {
+
+int64_t axb_ftable_bytes(int64_t kpad, int64_t coutp) {
+    if (kpad <= 0 || coutp <= 0 || kpad % 16 || coutp % 16) return 0;
+    return kpad * (coutp / 8) * kFtRowBytes;
+}
+
+int axb_ftable_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                       const axb_lut *lut, uint32_t *d_ftable, void *stream) {
+    if (!lut || !d_fcodes || !d_ftable) return set_error(AXB_E_VALUE, "null argument");
+    if (cs % 16 || c > cs || c < 1) return set_error(AXB_E_VALUE, "channel stride mismatch");
+    const int64_t kpad = axb_filter_kpad(kh, kw, cs), coutp = axb_filter_coutp(cout);
+    const int64_t total = (coutp / 8) * kpad * kFtRowWords;
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    ftable_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_fcodes, kpad, coutp, (int32_t)cs, (int32_t)c,
+                                                                  kh * kw * cs, lut->d_bmajor, lut->is_signed,
+                                                                  d_ftable);
+    return check_launch("ftable_prepare");
+}
+
+int axb_ft_variant_count(void) { return kNumFtVariants; }
+const char *axb_ft_variant_name(int v) { return (v >= 0 && v < kNumFtVariants) ? kFtVariants[v].name : ""; }
+
+}  // extern "C"

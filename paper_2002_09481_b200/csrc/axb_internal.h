@@ -15,4 +15,7 @@ int set_error(int code, const char *msg);
 int check_launch(const char *what);
 int sm_count();
 void set_last_kernel(const char *name);
+struct ConvK;
+// ftable kernel launch (axb_ftconv.cu); variant 0 = cost model
+int conv_ft_launch(const ConvK &k, int variant, int is_signed, int sm_limit, cudaStream_t s);
 }  // namespace axb

@@ -18,6 +18,8 @@ as a 1x1 over them.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -26,9 +28,12 @@ from .axconv import device_lut
 from .types import resolve_padding
 
 
+FTABLE_MAX_BYTES = 4 << 30  # per layer (ResNet-50's largest: 4608 x 512 x 512 B = 1.2 GB)
+
+
 class ConvLayer:
     def __init__(self, filters, f_range, lut, geometry, bias=None, round_mode="half-away-from-zero",
-                 accumulator="exact64", device=None, depthwise=False):
+                 accumulator="exact64", device=None, depthwise=False, ftable=None):
         self.lib = lib = _lib.load()
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
         f = np.ascontiguousarray(filters, dtype=np.float32)
@@ -70,6 +75,17 @@ class ConvLayer:
         if flags & _lib.FLAG_FSUM_OVF:
             raise OverflowError("filter size too large for 32-bit code sums")
         self.bias = None if bias is None else torch.from_numpy(np.ascontiguousarray(bias, np.float32)).to(self.device)
+        # filter-specialised product table (axb_ftable_prepare): 512 B per filter weight, built once
+        # per layer; the conv then gathers two channels' products per 32-bit shared-memory word
+        if ftable is None:
+            ftable = os.environ.get("AXB_FTABLE", "1") != "0"
+        nbytes = int(lib.axb_ftable_bytes(self.kpad, self.coutp))
+        self.ftable = None
+        if ftable and not self.depthwise and nbytes and self.kpad <= 32768 and fk[0] * fk[1] <= 256 \
+                and nbytes <= FTABLE_MAX_BYTES:
+            self.ftable = torch.empty(nbytes // 4, dtype=torch.int32, device=self.device)
+            _lib.check(lib.axb_ftable_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3], self.cout,
+                                              self.lut.handle, self.ftable.data_ptr(), stream))
         self.launches = 0
 
     def set_input_params(self, mn: float, mx: float) -> None:
@@ -81,7 +97,7 @@ class ConvLayer:
 
     def run(self, x: torch.Tensor, in_range_dev=None, *, relu=False, residual=None, out_range=None,
             out_flag=None, quant_flag=None, acc_out=None, force_generic=False, sm_limit=0, variant=0,
-            pixel_order=0, profile=None) -> torch.Tensor:
+            pixel_order=0, profile=None, ft_variant=0, use_ftable=True) -> torch.Tensor:
         """x: (n,h,w,cin) fp32 CUDA.  in_range_dev: device int32[2] ordered-float range, or None if
         set_input_params() was called.  Returns (n,oh,ow,cout) fp32."""
         lib = self.lib
@@ -149,6 +165,8 @@ class ConvLayer:
         d.sm_limit = int(sm_limit)
         d.variant = int(variant)
         d.pixel_order = int(pixel_order)
+        d.ftable = self.ftable.data_ptr() if (self.ftable is not None and use_ftable) else None
+        d.ft_variant = int(ft_variant)
         if profile is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()

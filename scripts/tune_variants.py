@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--variants", default="")
+    ap.add_argument("--family", default="ft", choices=["ft", "lut", "both"],
+                    help="ft: ftable-kernel variants; lut: b-major LUT kernel variants")
     ap.add_argument("--orders", default="", help="compare pixel orders (e.g. 1,4) at the heuristic variant")
     args = ap.parse_args()
     spec = workload_spec(args.workload, "trunc2")
@@ -39,9 +41,17 @@ def main():
     g = GpuGraph(spec["nodes"])
     trace = {}
     g.run(torch.from_numpy(imgs).cuda(), trace=trace)
-    nvar = _lib.load().axb_conv_variant_count()
-    variants = [int(v) for v in args.variants.split(",")] if args.variants else list(range(1, nvar))
-    names = [_lib.load().axb_conv_variant_name(v).decode() for v in range(nvar)]
+    lib = _lib.load()
+    runs = []  # (name, run kwargs)
+    if args.family in ("lut", "both"):
+        nvar = lib.axb_conv_variant_count()
+        vs = [int(v) for v in args.variants.split(",")] if args.variants else list(range(1, nvar))
+        runs += [(lib.axb_conv_variant_name(v).decode(), dict(variant=v, use_ftable=False)) for v in vs]
+    if args.family in ("ft", "both"):
+        nft = lib.axb_ft_variant_count()
+        runs += [(lib.axb_ft_variant_name(v).decode(), dict(ft_variant=v)) for v in range(1, nft)]
+        if args.family == "ft":
+            runs.append(("lut_auto", dict(use_ftable=False)))
     rows = []
     seen = set()
     for n in spec["nodes"]:
@@ -58,21 +68,21 @@ def main():
         flags = torch.zeros(2, dtype=torch.int32, device="cuda")
         res = {}
         ref = None
-        for v in variants:
+        for name, kw in runs:
             times = []
             for _ in range(6):
                 prof = []
-                y = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(), variant=v,
-                              profile=prof)
-                e0, e1, macs = prof[0]
+                y = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(), profile=prof,
+                              **kw)
+                e0, e1, macs = prof[0][:3]
                 torch.cuda.synchronize()
                 times.append(e0.elapsed_time(e1))
             t = statistics.median(times[1:])
             if ref is None:
                 ref = y
             elif not torch.equal(ref.view(torch.int32), y.view(torch.int32)):
-                raise SystemExit(f"variant {names[v]} differs on {n['id']}")
-            res[names[v]] = round(t, 4)
+                raise SystemExit(f"variant {name} differs on {n['id']}")
+            res[name] = round(t, 4)
         if args.orders:
             for o in [int(v) for v in args.orders.split(",")]:
                 if o == 4 and (y.shape[1] % 4 or y.shape[2] % 8):

@@ -28,7 +28,7 @@ def _lut(entries, mode):
     return T.MultLut(T.Signedness(mode), np.asarray(entries).astype(T.Signedness(mode).entry_dtype))
 
 
-def gpu_conv(case, acc=True, force_generic=False, sm_limit=0, variant=0):
+def gpu_conv(case, acc=True, force_generic=False, sm_limit=0, variant=0, ft_variant=0, use_ftable=True):
     """Run one case through ConvLayer (C-ABI stages: coeffs, quantize, [im2col], conv)."""
     torch = _torch()
     from paper_2002_09481_b200 import _lib
@@ -45,24 +45,56 @@ def gpu_conv(case, acc=True, force_generic=False, sm_limit=0, variant=0):
     if acc:
         acc_t = torch.empty(output_shape(case["x"].shape, case["f"].shape, geo), dtype=torch.int64, device="cuda")
     y = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(),
-                  force_generic=force_generic, sm_limit=sm_limit, variant=variant, acc_out=acc_t)
+                  force_generic=force_generic, sm_limit=sm_limit, variant=variant, acc_out=acc_t,
+                  ft_variant=ft_variant, use_ftable=use_ftable)
     torch.cuda.synchronize()
     kernel = _lib.last_kernel()
     return y.cpu().numpy(), (acc_t.cpu().numpy() if acc else None), kernel
 
 
-@pytest.mark.parametrize("generic", [False, True])
-def test_c1_cases_bit_exact(generic):
+@pytest.mark.parametrize("path", ["ftable", "lut", "generic"])
+def test_c1_cases_bit_exact(path):
+    """The reference's 100 acceptance cases (seed 2026) through each conv kernel family:
+    ftable (filter-specialised product table), lut (b-major LUT), generic (int64)."""
     g = load_golden("c1")
     rng = np.random.default_rng(2026)
     kernels = set()
     for i in range(100):
         case = random_conv_case(rng)
-        y, acc, kern = gpu_conv(case, force_generic=generic)
+        y, acc, kern = gpu_conv(case, force_generic=path == "generic", use_ftable=path == "ftable")
         kernels.add(kern.split("<")[0])
         assert bits_equal(y, g[f"out_{i}"]), (i, kern)
         assert np.array_equal(acc, g[f"acc_{i}"]), (i, kern)
-    assert (kernels == {"lutconv_generic"}) if generic else ("lutconv_generic" not in kernels)
+    if path == "generic":
+        assert kernels == {"lutconv_generic"}
+    elif path == "ftable":
+        assert any(k.startswith("ft") for k in kernels), kernels
+    else:
+        assert not any(k.startswith("ft") for k in kernels) and "lutconv_generic" not in kernels, kernels
+
+
+def test_all_ftable_variants_bit_identical():
+    """Every ftable-kernel tile variant gives the oracle's bits (outputs and raw sums), including
+    ragged pixel tiles, cout not a multiple of 16, residual + ReLU-free paths and both signedness."""
+    from paper_2002_09481_b200 import _lib
+
+    nvar = _lib.load().axb_ft_variant_count()
+    rng = np.random.default_rng(78)
+    cases = [random_conv_case(rng) for _ in range(16)]
+    for mode in (O.SIGNED, O.UNSIGNED):
+        big = dict(x=np.maximum(rng.standard_normal((5, 23, 21, 32)), 0).astype(np.float32),
+                   f=rng.standard_normal((3, 3, 32, 37)).astype(np.float32), lut=O.random_lut(rng, mode),
+                   mode=mode, padding="same", strides=(1, 1), dilations=(1, 1), accumulator=O.WRAP32,
+                   round_mode=O.HALF_EVEN)
+        big.update(in_range=(float(big["x"].min()), float(big["x"].max())),
+                   f_range=(float(big["f"].min()), float(big["f"].max())))
+        cases.append(big)
+    for case in cases:
+        want, want_acc = oracle_conv(case, return_acc=True)
+        for v in range(1, nvar):
+            y, acc, kern = gpu_conv(case, ft_variant=v)
+            assert bits_equal(y, want), (v, kern)
+            assert np.array_equal(acc, want_acc), (v, kern)
 
 
 def test_all_tile_variants_bit_identical():
