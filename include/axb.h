@@ -166,6 +166,8 @@ int64_t axb_ftable_bytes(int64_t kpad, int64_t coutp);
 int axb_ftable_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
                        const axb_lut *lut, uint32_t *d_ftable, void *stream);
 int axb_ft_variant_count(void);
+/* resident CTA clusters (CTAs for cluster size 1) of ftable variant v on the current device */
+int axb_ft_variant_clusters(int variant, int is_signed);
 const char *axb_ft_variant_name(int variant);
 int axb_conv_variant_count(void);
 /* Depthwise approximate conv (config 5; the reference has no groups): channel c

@@ -48,7 +48,11 @@ __host__ __device__ constexpr int ft_smem(int NPB, int KS, int ST) {
     return ST * ft_stage_bytes(NPB, KS) + kMaxTaps * 4 + 2 * ST * 8;
 }
 
-template <int TM, int WARPS, int NPB, int KS, int ST, bool SGN>
+// CL > 1: a thread-block cluster of CL CTAs works on CL pixel tiles of the SAME channel block in
+// lockstep; each CTA fetches 1/CL of every stage and multicasts it into all CL CTAs' rings (one L2
+// read per cluster instead of per CTA).  A slot is refilled once the warps of ALL CL CTAs released it
+// (the empty barrier counts CL*WARPS arrivals, made locally and through mapa'd remote arrives).
+template <int TM, int WARPS, int NPB, int KS, int ST, bool SGN, int CL>
 __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     constexpr int NT = WARPS * 32;
     constexpr int BM = NT * TM;
@@ -73,27 +77,44 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, WARPS);
+            mbar_init(empty + s, WARPS * CL);
         }
     }
     for (int t = tid; t < p.taps; t += NT) tapoff_s[t] = ((t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw) * p.cs;
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync();  // peers' barriers initialised before any remote arrive / multicast
+    const uint32_t rank = CL > 1 ? cluster_ctarank() : 0;
 
-    const int64_t grid = gridDim.x;
-    const int64_t my_tiles = p.ntiles > (int64_t)blockIdx.x ? (p.ntiles - blockIdx.x + grid - 1) / grid : 0;
+    // super-tile st = (channel block nb, pixel-tile group): CTA `rank` of the cluster takes pixel tile
+    // (st % ntm) * CL + rank (p.ntm = pixel-tile groups per channel block; tiles past the end are
+    // computed on pixel 0 and never stored)
+    const int64_t grid = gridDim.x / CL;  // clusters
+    const int64_t cid = blockIdx.x / CL;
+    const int64_t my_tiles = p.ntiles > cid ? (p.ntiles - cid + grid - 1) / grid : 0;
     const int64_t spt = (int64_t)p.nchunks * SPC;  // stages per tile
     const int64_t total = my_tiles * spt;
 
     // ---- producer (thread 0): stage h -> rows [q*KS, q*KS+KS) of tile pr_tile's channel block
-    int64_t pr_h = 0, pr_q = 0, pr_tile = blockIdx.x;
+    int64_t pr_h = 0, pr_q = 0, pr_tile = cid;
     auto produce = [&]() {
         const int slot = (int)(pr_h % ST);
         const int64_t nb = pr_tile / p.ntm;  // channel block of BN channels = NSUB sub-blocks
         mbar_expect_tx(full + slot, STAGE_BYTES);
+        // the stage = NSUB pieces (KS rows of one sub-block each); split into NPART equal parts,
+        // this CTA fetches parts rank, rank+CL, ... and multicasts them to the whole cluster
+        constexpr int NPART = NSUB > CL ? NSUB : CL;
+        constexpr int PPS = NPART / NSUB;  // parts per piece
+        constexpr uint32_t PART = STAGE_BYTES / NPART;
 #pragma unroll
-        for (int sb = 0; sb < NSUB; ++sb) {
-            const uint32_t *src = p.ftable + ((nb * NSUB + sb) * p.kpad + pr_q * KS) * kFtRowWords;
-            bulk_g2s(smem + slot * STAGE_BYTES + sb * (KS * kFtRowBytes), src, KS * kFtRowBytes, full + slot);
+        for (int part = (int)rank; part < NPART; part += CL) {
+            const int sb = part / PPS, q = part % PPS;
+            const uint32_t *src =
+                p.ftable + ((nb * NSUB + sb) * p.kpad + pr_q * KS + q * (KS / PPS)) * kFtRowWords;
+            uint8_t *dst = smem + slot * STAGE_BYTES + part * PART;
+            if constexpr (CL == 1)
+                bulk_g2s(dst, src, PART, full + slot);
+            else
+                bulk_g2s_multicast(dst, src, PART, full + slot, (uint16_t)((1u << CL) - 1));
         }
         ++pr_h;
         if (++pr_q == spt) {
@@ -107,7 +128,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     // ---- activation rows of this lane's TM pixels (int32 offsets: < 2 GiB per launch)
     int32_t rowbase[TM];
     auto set_rows = [&](int64_t tile) {
-        const int64_t m0 = (tile % p.ntm) * BM;
+        const int64_t m0 = ((tile % p.ntm) * CL + rank) * BM;
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
             const int64_t mt = m0 + warp * 32 * TM + i * 32 + lane;
@@ -143,7 +164,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     const int64_t bias_units = SGN ? (int64_t)32768 * p.kpad : 0;
 
     int64_t g = 0;  // consumer stage counter
-    int64_t c_tile = blockIdx.x;
+    int64_t c_tile = cid;
     if (my_tiles > 0) {
         set_rows(c_tile);
         load_chunk();
@@ -180,8 +201,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
             for (int st = 0; st < SPC; ++st) {
                 const int slot = (int)(g % ST);
                 if (tid == 0 && pr_h < total) {
-                    // refill the slot stage g-1 used, once every warp has released it
-                    if (g >= 1) mbar_wait(empty + (g - 1) % ST, (uint32_t)(((g - 1) / ST) & 1));
+                    // refill the slot stage g-1 used, once every warp (of every cluster CTA) released it.
+                    // (A non-blocking variant that skips the refill while a slow warp still holds the
+                    // slot measured slower: the pipeline lead in bytes is what matters.)
+                    if (g >= 1) {
+                        if constexpr (CL == 1)
+                            mbar_wait(empty + (g - 1) % ST, (uint32_t)(((g - 1) / ST) & 1));
+                        else
+                            mbar_wait_cluster(empty + (g - 1) % ST, (uint32_t)(((g - 1) / ST) & 1));
+                    }
                     produce();
                 }
                 mbar_wait(full + slot, (uint32_t)((g / ST) & 1));
@@ -205,7 +233,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty + slot);
+                if constexpr (CL == 1) {
+                    if (lane == 0) mbar_arrive(empty + slot);
+                } else if (lane < CL) {  // release the slot in every CTA of the cluster
+                    mbar_arrive_cluster(empty + slot, (uint32_t)lane);
+                }
 #pragma unroll
                 for (int i = 0; i < TM; ++i) {  // next stage's rows move to the front
                     if (KS == 4) {
@@ -223,7 +255,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
         {
             const EpiConst e = epi_const(p);
             const int64_t nb = c_tile / p.ntm;
-            const int64_t m0 = (c_tile % p.ntm) * BM;
+            const int64_t m0 = ((c_tile % p.ntm) * CL + rank) * BM;
             const int cb = (int)nb * BN;
             const bool full_blk = cb + BN <= p.cout && (p.cout & 3) == 0;
 #pragma unroll
@@ -297,6 +329,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     const bool any = tmin <= tmax;
     range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
                  AXB_FLAG_OUT_NONFINITE);
+    if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still arrive on its barriers
 }
 
 // ---------------------------------------------------------------- table preparation
@@ -329,72 +362,99 @@ __global__ void ftable_kernel(const uint8_t *__restrict__ fcodes, int64_t kpad, 
 // ---------------------------------------------------------------- host launch
 struct FtVariant {
     const char *name;
-    int tm, warps, npb;
+    int tm, warps, npb, cl;
     float cost;  // relative time per lookup slot (1 = best); tuned on B200
 };
 static const FtVariant kFtVariants[] = {
-    {"auto", 0, 0, 0, 0.f},
-    {"ft16_tm2_w16", 2, 16, 8, 1.00f},
-    {"ft16_tm4_w8", 4, 8, 8, 1.06f},
-    {"ft16_tm1_w16", 1, 16, 8, 1.20f},
-    {"ft8_tm4_w16", 4, 16, 4, 1.00f},
-    {"ft8_tm2_w16", 2, 16, 4, 1.05f},
-    {"ft8_tm4_w8", 4, 8, 4, 1.06f},
-    {"ft8_tm4_w16_k8", 4, 16, 4, 1.00f},
-    {"ft8_tm4_w16_k16", 4, 16, 4, 1.00f},
+    {"auto", 0, 0, 0, 0, 0.f},
+    {"ft16_tm2_w16_k8", 2, 16, 8, 1, 1.000f},
+    {"ft16_tm2_w16_k4", 2, 16, 8, 1, 1.110f},
+    {"ft8_tm4_w16_k16", 4, 16, 4, 1, 1.130f},
+    {"ft16_tm1_w16_k8", 1, 16, 8, 1, 1.145f},
+    {"ft8_tm2_w16_k16", 2, 16, 4, 1, 1.122f},
+    {"ft8_tm1_w8_k16", 1, 8, 4, 1, 1.537f},
+    {"ft16_tm2_w16_k8_c2", 2, 16, 8, 2, 1.177f},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
-template <int TM, int WARPS, int NPB, bool SGN, int KS = 4, int ST = 6>
-static int launch_ft(const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
+// op 0: launch; op 1: return how many CL-CTA clusters fit on the device at once (cached)
+template <int TM, int WARPS, int NPB, bool SGN, int CL, int KS = 4, int ST = 6>
+static int launch_ft(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WARPS * 32 * TM;
     constexpr int BN = 2 * NPB;
     const size_t smem = ft_smem(NPB, KS, ST);
-    auto fn = lutconv_ft<TM, WARPS, NPB, KS, ST, SGN>;
-    static int configured_dev = -1;
+    auto fn = lutconv_ft<TM, WARPS, NPB, KS, ST, SGN, CL>;
+    static int configured_dev = -1, max_clusters = 0;
     int dev = 0;
     cudaGetDevice(&dev);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(WARPS * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = CL > 1 ? 1 : 0;
     if (configured_dev != dev) {
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_ft");
+        max_clusters = sm_count();
+        if (CL > 1) {
+            cfg.gridDim = dim3(CL * (sm_count() / CL));
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n < 1) {
+                cudaGetLastError();
+                return set_error(AXB_E_CUDA, "no resident CTA cluster for lutconv_ft");
+            }
+            max_clusters = n;
+        }
         configured_dev = dev;
     }
+    if (op == 1) return max_clusters;
     ConvK kk = k;
-    kk.ntm = (int32_t)((k.M + BM - 1) / BM);
-    kk.ntiles = (int64_t)kk.ntm * (k.coutp / BN);
-    int64_t grid = sm_limit > 0 ? sm_limit : sm_count();
-    if (grid > kk.ntiles) grid = kk.ntiles;
-    if (grid < 1) grid = 1;
-    fn<<<(int)grid, WARPS * 32, smem, s>>>(kk);
+    const int64_t ntm = (k.M + BM - 1) / BM;
+    kk.ntm = (int32_t)((ntm + CL - 1) / CL);             // pixel-tile groups per channel block
+    kk.ntiles = (int64_t)kk.ntm * (k.coutp / BN);          // super-tiles
+    int64_t ncl = sm_limit > 0 ? (sm_limit / CL > 0 ? sm_limit / CL : 1) : max_clusters;
+    if (ncl > max_clusters) ncl = max_clusters;
+    if (ncl > kk.ntiles) ncl = kk.ntiles;
+    if (ncl < 1) ncl = 1;
+    cfg.gridDim = dim3((unsigned)(ncl * CL));
+    if (cudaLaunchKernelEx(&cfg, fn, kk) != cudaSuccess) return check_launch("lutconv_ft");
     set_last_kernel(name);
     return check_launch("lutconv_ft");
 }
 
 template <bool SGN>
-static int launch_ft_variant(int v, const ConvK &k, int sm_limit, cudaStream_t s) {
+static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaStream_t s) {
     const char *nm = kFtVariants[v].name;
     switch (v) {
-        case 1: return launch_ft<2, 16, 8, SGN>(k, sm_limit, s, nm);
-        case 2: return launch_ft<4, 8, 8, SGN>(k, sm_limit, s, nm);
-        case 3: return launch_ft<1, 16, 8, SGN>(k, sm_limit, s, nm);
-        case 4: return launch_ft<4, 16, 4, SGN>(k, sm_limit, s, nm);
-        case 5: return launch_ft<2, 16, 4, SGN>(k, sm_limit, s, nm);
-        case 6: return launch_ft<4, 8, 4, SGN>(k, sm_limit, s, nm);
-        case 7: return launch_ft<4, 16, 4, SGN, 8, 6>(k, sm_limit, s, nm);
-        case 8: return launch_ft<4, 16, 4, SGN, 16, 3>(k, sm_limit, s, nm);
+        case 1: return launch_ft<2, 16, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
+        case 2: return launch_ft<2, 16, 8, SGN, 1, 4, 6>(op, k, sm_limit, s, nm);
+        case 3: return launch_ft<4, 16, 4, SGN, 1, 16, 3>(op, k, sm_limit, s, nm);
+        case 4: return launch_ft<1, 16, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
+        case 5: return launch_ft<2, 16, 4, SGN, 1, 16, 3>(op, k, sm_limit, s, nm);
+        case 6: return launch_ft<1, 8, 4, SGN, 1, 16, 3>(op, k, sm_limit, s, nm);
+        case 7: return launch_ft<2, 16, 8, SGN, 2, 8, 3>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
 
-static int pick_ft_variant(const ConvK &k) {
-    const int64_t sms = sm_count();
+// time ~ cost * waves * BM * BN, waves = ceil(super-tiles / resident clusters)
+static int pick_ft_variant(const ConvK &k, int is_signed) {
     int best = 1;
     double best_t = 1e300;
     for (int v = 1; v < kNumFtVariants; ++v) {
         const FtVariant &x = kFtVariants[v];
+        const int64_t ncl = is_signed ? launch_ft_variant<true>(1, v, k, 0, 0) : launch_ft_variant<false>(1, v, k, 0, 0);
+        if (ncl < 1) continue;
         const int64_t bm = (int64_t)x.warps * 32 * x.tm, bn = 2 * x.npb;
-        const int64_t tiles = ((k.M + bm - 1) / bm) * (k.coutp / bn);
-        const int64_t waves = (tiles + sms - 1) / sms;
+        const int64_t ntm = (k.M + bm - 1) / bm;
+        const int64_t tiles = ((ntm + x.cl - 1) / x.cl) * (k.coutp / bn);
+        const int64_t waves = (tiles + ncl - 1) / ncl;
         const double t = (double)x.cost * (double)waves * (double)(bm * bn);
         if (t < best_t) {
             best_t = t;
@@ -407,8 +467,8 @@ static int pick_ft_variant(const ConvK &k) {
 int conv_ft_launch(const ConvK &k, int variant, int is_signed, int sm_limit, cudaStream_t s) {
     int v = variant;
     if (v < 0 || v >= kNumFtVariants) return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
-    if (v == 0) v = pick_ft_variant(k);
-    return is_signed ? launch_ft_variant<true>(v, k, sm_limit, s) : launch_ft_variant<false>(v, k, sm_limit, s);
+    if (v == 0) v = pick_ft_variant(k, is_signed);
+    return is_signed ? launch_ft_variant<true>(0, v, k, sm_limit, s) : launch_ft_variant<false>(0, v, k, sm_limit, s);
 }
 
 }  // namespace axb
@@ -439,6 +499,11 @@ int axb_ftable_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t 
 }
 
 int axb_ft_variant_count(void) { return kNumFtVariants; }
+int axb_ft_variant_clusters(int v, int is_signed) {
+    if (v < 1 || v >= kNumFtVariants) return set_error(AXB_E_VALUE, "unknown ftable kernel variant"), -1;
+    ConvK k{};
+    return is_signed ? launch_ft_variant<true>(1, v, k, 0, 0) : launch_ft_variant<false>(1, v, k, 0, 0);
+}
 const char *axb_ft_variant_name(int v) { return (v >= 0 && v < kNumFtVariants) ? kFtVariants[v].name : ""; }
 
 }  // extern "C"

@@ -1,0 +1,12 @@
+#!/bin/bash
+# ncu --set full captures of the ftable conv kernel: R8 s0b0.a/b, R50 (b64) s0b1.b, s2b1.b, s2b1.c
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+TAG=${TAG:-fp}
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lutconv_ft -s 1 -c 2 \
+    -o gpurun_out/prof_r8_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_r8_$TAG.log 2>&1
+for L in ${R50_LAUNCHES:-6 29}; do
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:lutconv -s $L -c 1 \
+    -o gpurun_out/prof_r50_l${L}_$TAG -f python bench.py --workload r50 --batch 64 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_r50_l${L}_$TAG.log 2>&1
+done
+if [ -n "$EXTRA" ]; then eval "$EXTRA"; fi; true
