@@ -325,12 +325,12 @@ def main():
         flush.zero_()
         run_all(x_dev, profile=profile)
     barrier()
-    conv_ms = sum(a.elapsed_time(b) for _, a, b, _, _ in profile) / args.steps
-    conv_macs = sum(m for _, _, _, m, _ in profile) / args.steps
-    conv_algo_bytes = sum(ab for *_, ab in profile) / args.steps
+    conv_ms = sum(a.elapsed_time(b) for _, a, b, _, _, _ in profile) / args.steps
+    conv_macs = sum(m for _, _, _, m, _, _ in profile) / args.steps
+    conv_algo_bytes = sum(ab for *_, ab, _ in profile) / args.steps
     conv_launches = len(profile) // args.steps
     layer_rows = {}
-    for nid, a, b, m, _ in profile:
+    for nid, a, b, m, _, _ in profile:
         r = layer_rows.setdefault(nid, [0.0, 0, 0])
         r[0] += a.elapsed_time(b)
         r[1] += m
@@ -380,7 +380,12 @@ def main():
         pass
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     max_mhz = float(peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0)
-    peak_lookups = sm_count * 32 * max_mhz * 1e6  # one 32-lane LDS wavefront per SM per clock
+    # Shared-memory lookup roofline of the product gather: 128 B per SM per clock (one wavefront of
+    # 32 four-byte banks) / 2 B per 16-bit product = 64 lookups/clk/SM.  The ftable kernel reaches it
+    # with two products per bank word; the north_star's LDS.16 roofline (one lookup per lane per
+    # wavefront, 32/clk/SM) is reported alongside.
+    peak_lookups = sm_count * 64 * max_mhz * 1e6
+    lds16_lookups = sm_count * 32 * max_mhz * 1e6
     achieved = conv_macs / (conv_ms / 1e3) if conv_ms else 0.0
     sampled = clocks.get("sm_mhz")
     traffic = None
@@ -390,12 +395,16 @@ def main():
             traffic = _json.loads(tf.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    kernels = sorted({k for *_, k in profile})
     roofline = {
-        "bound": "smem", "kernel": "lutconv_fast (LUT implicit GEMM, all conv launches of a step)",
+        "bound": "smem", "kernel": "LUT-product gather conv, all conv launches of a step: " + ", ".join(kernels),
         "achieved": round(achieved / 1e9, 2), "peak": round(peak_lookups / 1e9, 2), "unit": "Glookup/s",
         "frac": round(achieved / peak_lookups, 4),
-        "frac_at_sampled_clock": round(achieved / (sm_count * 32 * sampled * 1e6), 4) if sampled else None,
-        "peak_basis": f"derived: {sm_count} SMs x 32 lookups/clk x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+        "frac_at_sampled_clock": round(achieved / (sm_count * 64 * sampled * 1e6), 4) if sampled else None,
+        "peak_basis": f"derived: {sm_count} SMs x 128 B/clk shared-memory bandwidth / 2 B per 16-bit product "
+                      f"= 64 lookups/clk/SM x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+        "lds16_lookup_roofline": round(lds16_lookups / 1e9, 2),
+        "frac_vs_lds16_lookup_roofline": round(achieved / lds16_lookups, 4),
         "traffic": traffic, "traffic_unit": "DRAM bytes per LUT-conv launch (ncu --set full, committed profile)",
         "algorithmic_bytes_per_launch": int(conv_algo_bytes / max(conv_launches, 1)),
         "conv_launches_per_step": conv_launches,

@@ -150,3 +150,14 @@ def check(rc: int) -> None:
 
 def last_kernel() -> str:
     return (load().axb_last_kernel() or b"").decode()
+
+
+def kernel_family(variant_name: str) -> str:
+    """Kernel behind a variant name reported by axb_last_kernel()."""
+    if variant_name.startswith("ft"):
+        return "lutconv_ft"
+    if variant_name.startswith("lutconv_"):
+        return variant_name
+    if variant_name.startswith("depthwise"):
+        return variant_name
+    return "lutconv_fast"

@@ -52,7 +52,7 @@ __host__ __device__ constexpr int ft_smem(int NPB, int KS, int ST) {
 // lockstep; each CTA fetches 1/CL of every stage and multicasts it into all CL CTAs' rings (one L2
 // read per cluster instead of per CTA).  A slot is refilled once the warps of ALL CL CTAs released it
 // (the empty barrier counts CL*WARPS arrivals, made locally and through mapa'd remote arrives).
-template <int TM, int WARPS, int NPB, int KS, int ST, bool SGN, int CL>
+template <int TM, int WARPS, int NPB, int KS, int ST, bool SGN, int CL, int PF>
 __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     constexpr int NT = WARPS * 32;
     constexpr int BM = NT * TM;
@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     constexpr int SPC = 16 / KS;   // pipeline stages per 16-row chunk
     constexpr uint32_t STAGE_BYTES = ft_stage_bytes(NPB, KS);
     static_assert(NPB == 4 || NPB == 8, "4 or 8 channel pairs per tile");
+    static_assert(PF == 1 || PF == 2, "activation chunks loaded ahead: 1 or 2");
     static_assert(KS == 4 || KS == 8 || KS == 16, "KS rows per stage: 4, 8 or 16");
     static_assert(ft_smem(NPB, KS, ST) + 512 <= 232448, "ftable ring exceeds shared memory");
 
@@ -137,16 +138,25 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
             rowbase[i] = (int32_t)(pix0 * p.cs);
         }
     };
-    uint4 av[TM];
-    int ld_t = 0, ld_ci = 0;  // tap and channel offset of the next chunk to load
-    auto load_chunk = [&]() {
+    // loader: runs PF chunks ahead of the consumer, across tile boundaries
+    uint4 av[PF][TM];
+    int ld_t = 0, ld_ci = 0, ld_kc = 0;  // tap, channel offset and index of the next chunk to load
+    int64_t ld_left = my_tiles * p.nchunks, ld_tile = cid;
+    auto load_next = [&](uint4(&dst)[TM]) {
+        if (ld_left == 0) return;
         const int off = tapoff_s[ld_t] + ld_ci;
 #pragma unroll
-        for (int i = 0; i < TM; ++i) av[i] = __ldg(reinterpret_cast<const uint4 *>(p.codes + rowbase[i] + off));
+        for (int i = 0; i < TM; ++i) dst[i] = __ldg(reinterpret_cast<const uint4 *>(p.codes + rowbase[i] + off));
+        --ld_left;
         ld_ci += 16;
         if (ld_ci == p.cs) {
             ld_ci = 0;
             ++ld_t;
+        }
+        if (++ld_kc == p.nchunks) {
+            ld_kc = ld_t = ld_ci = 0;
+            ld_tile += grid;
+            if (ld_left > 0) set_rows(ld_tile);
         }
     };
 
@@ -167,21 +177,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     int64_t c_tile = cid;
     if (my_tiles > 0) {
         set_rows(c_tile);
-        load_chunk();
+#pragma unroll
+        for (int q = 0; q < PF; ++q) load_next(av[q]);
     }
     for (int64_t jt = 0; jt < my_tiles; ++jt) {
 #pragma unroll 1
         for (int kc = 0; kc < p.nchunks; ++kc) {
             uint4 cur[TM];
 #pragma unroll
-            for (int i = 0; i < TM; ++i) cur[i] = av[i];
-            if (kc + 1 < p.nchunks) {
-                load_chunk();
-            } else if (jt + 1 < my_tiles) {  // first chunk of the next tile, during this tile's last chunk
-                ld_t = ld_ci = 0;
-                set_rows(c_tile + grid);
-                load_chunk();
+            for (int i = 0; i < TM; ++i) {
+                cur[i] = av[0][i];
+                if (PF == 2) av[0][i] = av[PF - 1][i];
             }
+            load_next(av[PF - 1]);
             // S_p += the 16 code values (junk codes are raw 0 -> value 0), axconv.py:193
 #pragma unroll
             for (int i = 0; i < TM; ++i) {
@@ -368,22 +376,22 @@ struct FtVariant {
 static const FtVariant kFtVariants[] = {
     {"auto", 0, 0, 0, 0, 0.f},
     {"ft16_tm2_w16_k8", 2, 16, 8, 1, 1.000f},
-    {"ft16_tm2_w16_k4", 2, 16, 8, 1, 1.110f},
-    {"ft8_tm4_w16_k16", 4, 16, 4, 1, 1.130f},
-    {"ft16_tm1_w16_k8", 1, 16, 8, 1, 1.145f},
-    {"ft8_tm2_w16_k16", 2, 16, 4, 1, 1.122f},
-    {"ft8_tm1_w8_k16", 1, 8, 4, 1, 1.537f},
-    {"ft16_tm2_w16_k8_c2", 2, 16, 8, 2, 1.177f},
+    {"ft16_tm2_w16_k4", 2, 16, 8, 1, 1.105f},
+    {"ft8_tm4_w16_k16", 4, 16, 4, 1, 1.139f},
+    {"ft16_tm1_w16_k8", 1, 16, 8, 1, 1.095f},
+    {"ft8_tm2_w16_k16", 2, 16, 4, 1, 1.127f},
+    {"ft8_tm1_w8_k16", 1, 8, 4, 1, 1.556f},
+    {"ft16_tm2_w16_k8_c2", 2, 16, 8, 2, 1.219f},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
 // op 0: launch; op 1: return how many CL-CTA clusters fit on the device at once (cached)
-template <int TM, int WARPS, int NPB, bool SGN, int CL, int KS = 4, int ST = 6>
+template <int TM, int WARPS, int NPB, bool SGN, int CL, int KS = 4, int ST = 6, int PF = 1>
 static int launch_ft(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WARPS * 32 * TM;
     constexpr int BN = 2 * NPB;
     const size_t smem = ft_smem(NPB, KS, ST);
-    auto fn = lutconv_ft<TM, WARPS, NPB, KS, ST, SGN, CL>;
+    auto fn = lutconv_ft<TM, WARPS, NPB, KS, ST, SGN, CL, PF>;
     static int configured_dev = -1, max_clusters = 0;
     int dev = 0;
     cudaGetDevice(&dev);

@@ -177,7 +177,11 @@ class ConvLayer:
             e1.record()
             # algorithmic HBM bytes of the conv launch: codes (+ per-pixel sums), filter codes,
             # fp32 output, residual read
-            algo = d.n * d.hp * d.wp * (d.cs + 4) + self.kpad * self.coutp + n * oh * ow * self.cout * (
-                8 if residual is not None else 4)
-            profile.append((e0, e1, n * oh * ow * self.kh * self.kw * c * self.cout, algo))
+            # algorithmic HBM bytes of the conv launch: codes (+ per-pixel sums), filter codes or the
+            # filter-specialised product table (read once), fp32 output, residual read
+            ft = d.ftable is not None
+            algo = d.n * d.hp * d.wp * (d.cs + 4) + (self.ftable.numel() * 4 if ft else self.kpad * self.coutp) \
+                + n * oh * ow * self.cout * (8 if residual is not None else 4)
+            profile.append((e0, e1, n * oh * ow * self.kh * self.kw * c * self.cout, algo,
+                            _lib.kernel_family(_lib.last_kernel())))
         return out

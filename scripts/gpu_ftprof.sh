@@ -10,3 +10,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:lutc
     -o gpurun_out/prof_r50_l${L}_$TAG -f python bench.py --workload r50 --batch 64 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_r50_l${L}_$TAG.log 2>&1
 done
 if [ -n "$EXTRA" ]; then eval "$EXTRA"; fi; true
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:lutconv -c 10 \
+    --csv --log-file gpurun_out/traffic_r8.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:lutconv -c 54 \
+    --csv --log-file gpurun_out/traffic_r50.csv python bench.py --workload r50 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r8_$TAG.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
