@@ -74,7 +74,8 @@ def workload_spec(name: str, lut_kind: str):
                     desc="ResNet-50 v1.5 224x224 (53 convs + 1x1 AxConv2D classifier), BN folded")
     if name == "r62sweep":
         return dict(nodes=resnet.cifar_resnet(10, sweep_luts()[0], seed=0), batch=1000, kind="cifar",
-                    lut="32 candidates: truncated_lut(mode, d) d=0..7 x {signed, unsigned} + 16 random_lut",
+                    lut="32 candidates: truncated_lut(mode, d) d=0..7 x {signed, unsigned} + 16 perturbed_lut "
+                        "(exact + uniform error of 2..256, both signedness)",
                     desc="ResNet-62 CIFAR-10 multiplier sweep over 32 candidate tables (config 4)",
                     sweep=True)
     raise SystemExit(f"unknown workload {name}")
@@ -84,9 +85,11 @@ def sweep_luts():
     """Config 4's 32 candidate multipliers."""
     from paper_2002_09481_b200 import types as T
 
+    # 16 truncated multipliers + 16 error-injected ones (uniform random tables, as in the reference's
+    # test helper, drive a 63-conv network to non-finite activations -> ValueError, graph.py:273-274)
     luts = [T.truncated_lut(m, d) for m in (T.Signedness.SIGNED, T.Signedness.UNSIGNED) for d in range(8)]
-    luts += [T.random_lut(np.random.default_rng(5000 + i), T.Signedness.SIGNED if i % 2 else T.Signedness.UNSIGNED)
-             for i in range(16)]
+    luts += [T.perturbed_lut(np.random.default_rng(5000 + i), T.Signedness.SIGNED if i % 2 else T.Signedness.UNSIGNED,
+                             1 + i // 2) for i in range(16)]
     return luts
 
 

@@ -274,6 +274,18 @@ def truncated_lut(mode, drop_bits: int) -> MultLut:
     return MultLut(m, np.multiply.outer(t, t).ravel().astype(m.entry_dtype))
 
 
+def perturbed_lut(rng: np.random.Generator, mode, err_bits: int) -> MultLut:
+    """Exact products plus a uniform integer error in [-2^err_bits, 2^err_bits] per entry, clipped to
+    the 16-bit entry range: a stand-in for a characterised approximate multiplier (error-injected
+    candidate for multiplier sweeps; a uniform random table makes deep networks diverge)."""
+    m = mode if isinstance(mode, Signedness) else Signedness(_mode_value(mode))
+    v = _operand_values(m)
+    exact = np.multiply.outer(v, v).ravel().astype(np.int64)
+    e = rng.integers(-(1 << err_bits), (1 << err_bits) + 1, exact.size)
+    lo, hi = (-(1 << 15), (1 << 15) - 1) if m is Signedness.SIGNED else (0, (1 << 16) - 1)
+    return MultLut(m, np.clip(exact + e, lo, hi).astype(m.entry_dtype))
+
+
 def random_lut(rng: np.random.Generator, mode) -> MultLut:
     """Uniform random 16-bit table (the reference tests' generator, cases.py:25-30)."""
     m = mode if isinstance(mode, Signedness) else Signedness(_mode_value(mode))
