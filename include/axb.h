@@ -21,6 +21,7 @@
  *                              (:160-196, implicit) + graph.py:268-277 bias / ReLU epilogue
  *   axb_axconv2d            <- axconv.py:266-297  axconv2d (whole operator, one call)
  *   axb_maxpool/avgpool     <- graph.py:182-199   _pool2d (float glue around the op)
+ *   axb_cifar_decode        <- formats.py:138-157 load_cifar10 (decode on device) + the input range
  *   axb_add_relu            <- graph.py:276-286   ReLU / Add nodes
  */
 #ifndef AXB_H
@@ -42,6 +43,7 @@ extern "C" {
 #define AXB_FLAG_PSUM_OVF 2       /* patch code sum outside int32 (OverflowError)           */
 #define AXB_FLAG_OUT_NONFINITE 4  /* non-finite kernel output feeding a fused range         */
 #define AXB_FLAG_FSUM_OVF 8       /* filter code sum outside int32 (OverflowError)          */
+#define AXB_FLAG_LABEL 16         /* CIFAR-10 label byte outside 0..9 (FormatError)         */
 
 /* signedness / rounding / accumulator enums (quantizer.py:28-49, axconv.py:47-58) */
 #define AXB_UNSIGNED 0
@@ -197,6 +199,14 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
                  int32_t pb, int32_t pl, int32_t pr, double in_min, double in_max, double f_min,
                  double f_max, int32_t round_mode, int32_t accumulator, const axb_lut *lut, float *d_out,
                  int64_t *d_acc_out, void *stream);
+
+/* ---- device ingest of CIFAR-10 binary records (formats.py:138-157) --------- */
+/* d_records: n x 3,073 bytes (label + R, G, B planes of 32x32).  d_images: (n,32,32,3)
+ * fp32 NHWC = float32(byte)/255; d_labels (nullable): n bytes.  d_range (nullable):
+ * ordered-float [min,max] of the images accumulated (reset it first), the graph input's
+ * Min/Max nodes.  A label byte > 9 sets AXB_FLAG_LABEL in d_flags (nullable). */
+int axb_cifar_decode(const uint8_t *d_records, int64_t n, float *d_images, uint8_t *d_labels, int32_t *d_range,
+                     int32_t *d_flags, void *stream);
 
 /* ---- float glue for the graph executor ------------------------------------ */
 int axb_maxpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t ph, int32_t pw,

@@ -22,6 +22,7 @@ FLAG_NONFINITE = 1
 FLAG_PSUM_OVF = 2
 FLAG_OUT_NONFINITE = 4
 FLAG_FSUM_OVF = 8
+FLAG_LABEL = 16
 
 UNSIGNED = 0
 SIGNED = 1
@@ -105,6 +106,7 @@ SIGNATURES = {
     "axb_avgpool": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                             c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "axb_add_relu": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "axb_cifar_decode": (c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 
 _lib = None

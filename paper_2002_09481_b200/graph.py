@@ -33,6 +33,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .formats import CIFAR_RECORD_BYTES, FormatError
 from .layer import ConvLayer
 from .types import ConvGeometry, _mode_value, output_shape, resolve_padding
 
@@ -93,6 +94,8 @@ class GpuGraph:
         self.sm_limit = int(sm_limit)
         self.variant = int(variant)
         self.lib = _lib.load()
+        self.labels = None  # device labels of the last record batch
+        self._slot_sets = {}  # (input shape, dtype) -> captured CUDA-graph slots
         self._plan()
 
     # ------------------------------------------------------------------ planning
@@ -234,10 +237,18 @@ class GpuGraph:
         ``profile`` (a list) receives (node_id, start_event, end_event, macs)
         around every LUT-conv kernel launch, for live per-kernel timing.
         """
-        if batch.dim() != 4:
-            raise ValueError("batch must be NHWC")
-        batch = batch.to(self.device, torch.float32).contiguous()
-        self._prepare_shapes(tuple(batch.shape))
+        records = batch.dtype == torch.uint8
+        if records:  # CIFAR-10 binary records (n, 3073): decoded on the device (formats.py:138-157)
+            if batch.dim() != 2 or batch.shape[1] != CIFAR_RECORD_BYTES:
+                raise ValueError(f"record batch must be (n, {CIFAR_RECORD_BYTES}) uint8")
+            batch = batch.to(self.device).contiguous()
+            in_shape = (int(batch.shape[0]), 32, 32, 3)
+        else:
+            if batch.dim() != 4:
+                raise ValueError("batch must be NHWC")
+            batch = batch.to(self.device, torch.float32).contiguous()
+            in_shape = tuple(batch.shape)
+        self._prepare_shapes(in_shape)
         lib = self.lib
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self.ranges.copy_(self.ranges_template)
@@ -269,7 +280,17 @@ class GpuGraph:
         for st in self.steps:
             n = st.node
             nid = n["id"]
-            if st.kind == "Input":
+            if st.kind == "Input" and records:
+                images = torch.empty(in_shape, dtype=torch.float32, device=self.device)
+                if self.labels is None or self.labels.numel() != in_shape[0]:
+                    self.labels = torch.empty(in_shape[0], dtype=torch.uint8, device=self.device)
+                if in_shape[0] == 0 and nid in self.need_range:
+                    raise ValueError("cannot take the range of an empty tensor")
+                _lib.check(lib.axb_cifar_decode(batch.data_ptr(), in_shape[0], images.data_ptr(),
+                                                self.labels.data_ptr(), rng_ptr(nid), flag_ptr(nid), stream))
+                self.launches += 1
+                vals[nid] = images
+            elif st.kind == "Input":
                 vals[nid] = batch
                 if nid in self.need_range:
                     if batch.numel() == 0:
@@ -335,7 +356,7 @@ class GpuGraph:
         self._check_flag_array(self.flags.cpu().numpy())
 
     # ------------------------------------------------------------------ CUDA graphs + pipelined host I/O
-    def capture(self, in_shape, slots: int = 2) -> None:
+    def capture(self, in_shape, slots: int = 2, dtype=torch.float32) -> None:
         """Record ``run`` for a fixed input shape into ``slots`` CUDA graphs (one per static
         input buffer).  Replays launch the whole step (range, quantize, LUT convs, pools, ...)
         with one CPU call; each slot owns its input buffer, output and flag snapshot, so a
@@ -345,9 +366,10 @@ class GpuGraph:
         side = torch.cuda.Stream(self.device)
         side.wait_stream(stream)
         self._slots = []
+        self._slot_sets[(in_shape, dtype)] = self._slots
         with torch.cuda.stream(side):
             for _ in range(slots):
-                x = torch.zeros(in_shape, dtype=torch.float32, device=self.device)
+                x = torch.zeros(in_shape, dtype=dtype, device=self.device)
                 self.run(x, check=False)  # warm-up: filter prep, shared-memory attributes, allocator
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=side):
@@ -360,6 +382,7 @@ class GpuGraph:
 
     def replay(self, batch: torch.Tensor, slot: int = 0, check: bool = True) -> torch.Tensor:
         """One step through the captured graph of ``slot`` (batch copied into its static input)."""
+        self._select_slots(batch)
         sl = self._slots[slot]
         sl["x"].copy_(batch, non_blocking=True)
         sl["graph"].replay()
@@ -367,12 +390,19 @@ class GpuGraph:
             self._check_flag_array(sl["flags"].cpu().numpy())
         return sl["y"]
 
+    def _select_slots(self, batch) -> bool:
+        sl = self._slot_sets.get((tuple(int(v) for v in batch.shape), batch.dtype))
+        if sl is not None:
+            self._slots = sl
+        return sl is not None
+
     def run_pipelined(self, host_batches, host_outputs=None, before_step=None):
         """End-to-end over pinned HOST batches: H2D of step i+1 (copy stream) overlaps the
-        captured compute of step i; each step's logits and flags come back D2H.  Returns the
-        list of host outputs; raises like ``run`` if any step saw non-finite values."""
-        if not getattr(self, "_slots", None):
-            self.capture(host_batches[0].shape)
+        captured compute of step i; each step's logits and flags come back D2H.  Host batches
+        are NHWC fp32 images or (n, 3073) uint8 CIFAR-10 records (decoded on the device).
+        Returns the list of host outputs; raises like ``run`` if any step saw non-finite values."""
+        if not self._select_slots(host_batches[0]):
+            self.capture(host_batches[0].shape, dtype=host_batches[0].dtype)
         nsl = len(self._slots)
         comp = torch.cuda.current_stream(self.device)
         copy = torch.cuda.Stream(self.device)
@@ -409,6 +439,8 @@ class GpuGraph:
         return outs
 
     def _check_flag_array(self, fl):
+        if fl.any() and (np.asarray(fl) & _lib.FLAG_LABEL).any():
+            raise FormatError("label byte outside 0..9")
         for n in self.nodes:
             if n["kind"] in ("Min", "Max"):
                 tid = self.t(n["inputs"][0])

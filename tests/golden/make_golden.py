@@ -19,6 +19,9 @@ Fixtures:
   nets.npz   end-to-end logits (and per-conv output sha256) of our ResNet-8 /
              ResNet-62 / ResNet-50 graphs run through the reference
              ``graph.run`` (engine "gemm").
+  formats.npz  bytes the reference's axemu.formats writes / decodes: .axm sha256s,
+             a .axt file, a 6-record CIFAR-10 file + its decoded images/labels,
+             a report CSV (``--formats`` regenerates only this one).
 """
 
 from __future__ import annotations
@@ -243,7 +246,40 @@ def make_nets() -> dict:
     return out
 
 
+def make_formats() -> dict:
+    """Bytes written / decoded by the reference's axemu.formats (formats.py:58-255)."""
+    import tempfile
+
+    from axemu import (load_cifar10, make_report, report_csv, save_cifar10, save_lut, save_tensor,
+                       synthetic_cifar10)
+
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        td = Path(td)
+        for tag, lut in (("exact_unsigned", exact_lut(Signedness.UNSIGNED)),
+                         ("trunc3_signed", truncated_lut(Signedness.SIGNED, 3))):
+            save_lut(lut, td / f"{tag}.axm")
+            out[f"lut_{tag}_sha"] = np.frombuffer(bytes.fromhex(hashlib.sha256(
+                (td / f"{tag}.axm").read_bytes()).hexdigest()), np.uint8)
+        t = Tensor4(np.array([0.0, 0.5, -1.25, 3.0], np.float32).reshape(1, 2, 2, 1))
+        save_tensor(t, td / "unit.axt")
+        out["tensor_unit_bytes"] = np.frombuffer((td / "unit.axt").read_bytes(), np.uint8)
+        images, labels = synthetic_cifar10(6, seed=3)
+        save_cifar10(td / "b.bin", images, labels)
+        out["cifar_records"] = np.frombuffer((td / "b.bin").read_bytes(), np.uint8)
+        batch = load_cifar10(td / "b.bin")
+        out["cifar_images"] = batch.images.data
+        out["cifar_labels"] = batch.labels
+        rep = make_report(0.25, 1.5, 0.75, 0.5, 123456, {"conv1": 0.4, "conv2": 0.35})
+        out["report_csv"] = np.frombuffer(report_csv(rep).encode(), np.uint8)
+    return out
+
+
 def main():
+    if "--formats" in sys.argv:
+        np.savez_compressed(HERE / "formats.npz", **make_formats())
+        print("formats ok", flush=True)
+        return
     c1 = make_c1()
     np.savez_compressed(HERE / "c1.npz", **c1)
     print("c1 ok", flush=True)
@@ -253,6 +289,8 @@ def main():
     nets = make_nets()
     np.savez_compressed(HERE / "nets.npz", **nets)
     print("nets ok", flush=True)
+    np.savez_compressed(HERE / "formats.npz", **make_formats())
+    print("formats ok", flush=True)
 
 
 if __name__ == "__main__":

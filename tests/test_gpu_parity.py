@@ -454,3 +454,69 @@ def test_quantizer_fast_path_sweep():
             assert np.array_equal(pixsum.cpu().numpy(), want2.reshape(n, c).astype(np.int32).sum(1))
             pb = prm2.cpu().numpy()
             assert pb[:8].view(np.float64)[0] == s2 and pb[8:12].view(np.int32)[0] == zp2
+
+
+def test_cifar_decode_kernel_matches_reference_decode():
+    """axb_cifar_decode == the reference's load_cifar10 decode (formats.py:138-157) bit for bit,
+    with the fused input range and the label check."""
+    torch = _torch()
+    from paper_2002_09481_b200 import _lib
+    from paper_2002_09481_b200 import formats as F
+    from paper_2002_09481_b200.datasets import synthetic_cifar10
+
+    lib = _lib.load()
+    g = load_golden("formats")
+    imgs, labels = synthetic_cifar10(1000, seed=4)
+    for rec, want_img, want_lab in ((g["cifar_records"].reshape(-1, 3073), g["cifar_images"], g["cifar_labels"]),
+                                    (F.encode_cifar10(imgs, labels), imgs, labels)):
+        n = rec.shape[0]
+        d_rec = torch.from_numpy(np.ascontiguousarray(rec)).cuda()
+        out = torch.empty((n, 32, 32, 3), dtype=torch.float32, device="cuda")
+        lab = torch.empty(n, dtype=torch.uint8, device="cuda")
+        rng = torch.tensor([2**31 - 1, -(2**31)], dtype=torch.int32, device="cuda")
+        flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(lib.axb_cifar_decode(d_rec.data_ptr(), n, out.data_ptr(), lab.data_ptr(), rng.data_ptr(),
+                                        flags.data_ptr(), None))
+        torch.cuda.synchronize()
+        assert bits_equal(out.cpu().numpy(), want_img)
+        assert np.array_equal(lab.cpu().numpy(), want_lab)
+        mn, mx = (float(np.float32(v)) for v in (want_img.min(), want_img.max()))
+        r = rng.cpu().numpy()
+        got = [np.int32(v) for v in r]
+        ords = [int(v) if v >= 0 else int(v) ^ 0x7FFFFFFF for v in got]
+        assert np.array(ords, np.int32).view(np.float32).tolist() == [mn, mx]
+        assert int(flags.item()) == 0
+    bad = np.zeros((3, 3073), np.uint8)
+    bad[2, 0] = 12
+    d_rec = torch.from_numpy(bad).cuda()
+    out = torch.empty((3, 32, 32, 3), dtype=torch.float32, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(lib.axb_cifar_decode(d_rec.data_ptr(), 3, out.data_ptr(), None, None, flags.data_ptr(), None))
+    assert int(flags.item()) & _lib.FLAG_LABEL
+
+
+def test_graph_on_cifar_records_matches_images():
+    """GpuGraph fed CIFAR-10 records (device decode, fused range) gives the same logits bits as
+    fed the decoded fp32 images -- eagerly, replayed, and through run_pipelined from host."""
+    torch = _torch()
+    from paper_2002_09481_b200 import formats as F
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.datasets import synthetic_cifar10
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    imgs, labels = synthetic_cifar10(96, seed=21)
+    rec = F.encode_cifar10(imgs, labels)
+    g = GpuGraph(resnet.cifar_resnet(1, T.truncated_lut(T.Signedness.SIGNED, 2), seed=0))
+    want = g.run(torch.from_numpy(imgs).cuda()).cpu().numpy()
+    got = g.run(torch.from_numpy(rec).cuda()).cpu().numpy()
+    assert bits_equal(got, want)
+    assert np.array_equal(g.labels.cpu().numpy(), labels)
+    hosts = [torch.from_numpy(rec).pin_memory() for _ in range(3)]
+    outs = g.run_pipelined(hosts)
+    for o in outs:
+        assert bits_equal(o.numpy(), want)
+    bad = rec.copy()
+    bad[5, 0] = 11
+    with pytest.raises(F.FormatError, match="label"):
+        g.run(torch.from_numpy(bad).cuda())
