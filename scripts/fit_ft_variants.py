@@ -21,10 +21,10 @@ SMS = 148
 
 
 def parse(name):
-    m = re.match(r"ft(\d+)_tm(\d+)_w(\d+)_k(\d+)(?:_c(\d+))?$", name)
+    m = re.match(r"ft(\d+)(r?)_tm(\d+)_w(\d+)(?:_k(\d+))?(?:_c(\d+))?$", name)
     if not m:
         return None
-    return int(m.group(1)), int(m.group(2)), int(m.group(3)), int(m.group(5) or 1)
+    return int(m.group(1)), int(m.group(3)), int(m.group(4)), int(m.group(6) or 1), m.group(2) == "r"
 
 
 def geom(r):
@@ -35,8 +35,12 @@ def geom(r):
 
 
 def base(name, m, coutp):
-    bn, tm, warps, cl = parse(name)
+    bn, tm, warps, cl, res = parse(name)
     bm = warps * 32 * tm
+    if res:  # fixed channel block per CTA
+        ntb, ntm = coutp // bn, math.ceil(m / bm)
+        per = min(SMS // ntb, ntm)
+        return math.ceil(ntm / per) * bm * bn
     tiles = math.ceil(math.ceil(m / bm) / cl) * (coutp // bn)
     return math.ceil(tiles / (SMS // cl)) * bm * bn
 
@@ -68,7 +72,7 @@ def main():
         def sub(mo):
             return mo.group(1) + f"{cost[mo.group(2)]:.3f}f" if mo.group(2) in cost else mo.group(0)
 
-        src = re.sub(r'(\{"(ft\d+_tm\d+_w\d+_k\d+(?:_c\d+)?)", \d+, \d+, \d+, \d+, )\d+\.\d+f', sub, src)
+        src = re.sub(r'(\{"(ft\d+r?_tm\d+_w\d+(?:_k\d+)?(?:_c\d+)?)", \d+, \d+, \d+, \d+, )\d+\.\d+f', sub, src)
         CU.write_text(src)
         print("patched", CU)
 
