@@ -16,6 +16,7 @@
  *   axb_coeffs_host         <- quantizer.py:98-117 compute_coeffs (host scalars)
  *   axb_quantize_pad        <- quantizer.py:120-131 quantize_values + axconv.py:181-189 zp padding
  *   axb_quantize_pad_range  <- the two above fused (coefficients of a device range, then quantize)
+ *   axb_quantize_im2col     <- quantize_values + zp padding + im2cols (axconv.py:160-196) in one pass
  *   axb_filters_prepare     <- axconv.py:199-210  quantize_filters (K x Cout codes + S_f)
  *   axb_conv2d_lut          <- axconv.py:213-257  approx_gemm/_lut_matmul (:136-146) + im2cols
  *                              (:160-196, implicit) + graph.py:268-277 bias / ReLU epilogue
@@ -189,6 +190,14 @@ int64_t axb_conv_im2col_kp(int64_t c, int64_t kh, int64_t kw);
 int axb_im2col_pack(const uint8_t *d_codes, int64_t n, int64_t hp, int64_t wp, int64_t cs, int64_t c, int32_t kh,
                     int32_t kw, int32_t sh, int32_t sw, int32_t dh, int32_t dw, int64_t oh, int64_t ow, int64_t kp,
                     int is_signed, uint8_t *d_rows, int32_t *d_rowsum, void *stream);
+/* The same rows straight from the fp32 input (quantize_values + zp padding + im2cols in one
+ * pass; the zp-padded code tensor is never written).  d_range non-null: coefficients of that
+ * device range computed in the kernel (written to d_params, as axb_quantize_pad_range);
+ * NULL: d_params holds host-computed parameters (as axb_quantize_pad). */
+int axb_quantize_im2col(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pl,
+                        int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t dh, int32_t dw, int64_t oh, int64_t ow,
+                        int64_t kp, const int32_t *d_range, axb_qparams *d_params, int is_signed, int round_mode,
+                        uint8_t *d_rows, int32_t *d_rowsum, int32_t *d_flags, void *stream);
 /* which kernel variant the last axb_conv2d_lut call on this thread launched */
 const char *axb_last_kernel(void);
 

@@ -98,6 +98,9 @@ SIGNATURES = {
     "axb_conv_im2col_kp": (c_i64, [c_i64, c_i64, c_i64]),
     "axb_im2col_pack": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
                                 c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_vp]),
+    "axb_quantize_im2col": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                    c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_int, c_int, c_vp, c_vp, c_vp,
+                                    c_vp]),
     "axb_axconv2d": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i32, c_i32,
                              c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_dbl, c_dbl, c_dbl, c_dbl, c_i32,
                              c_i32, c_vp, c_vp, c_vp, c_vp]),

@@ -470,6 +470,75 @@ __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t *__restr
     }
 }
 
+// ---------------------------------------------------------------- fused quantize + im2col (small-c layers)
+// One thread per output row: quantizes the kh*kw*c fp32 inputs of its window straight into
+// the kp-byte code row (zero-point code for padding taps, raw 0 beyond K) and writes the row
+// sum S_p -- the codes tensor of quantize_pad is never materialised.  Same per-element
+// arithmetic as quantize_pad16_kernel (fp32 estimate, exact fallback near ties / non-finite).
+__global__ void __launch_bounds__(256) quantize_im2col_kernel(
+    const float *__restrict__ x, int n, int h, int w, int c, int pt, int pl, int kh, int kw, int sh, int sw, int dh,
+    int dw, int oh, int ow, FastDiv fd_oh, FastDiv fd_ow, int kp, axb_qparams *prm, const int32_t *d_range,
+    int is_signed, int round_mode, uint8_t *__restrict__ rows, int32_t *__restrict__ rowsum, int32_t *d_flags) {
+    __shared__ QuantCtx q;
+    if (d_range)
+        quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
+    else
+        quant_ctx_load(q, prm, is_signed);
+    const bool nearest = round_mode != AXB_ROUND_TOWARD_ZERO;
+    const int lo = q.lo;
+    const uint32_t zpraw = (uint32_t)(q.zp & 0xFF);
+    const int K = kh * kw * c;
+    int nonfinite = 0;
+    const uint32_t total = (uint32_t)n * (uint32_t)oh * (uint32_t)ow;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < total; r += gridDim.x * blockDim.x) {
+        const uint32_t t = fdiv(r, fd_ow);
+        const int ox = (int)(r - t * (uint32_t)ow);
+        const uint32_t b = fdiv(t, fd_oh);
+        const int oy = (int)(t - b * (uint32_t)oh);
+        const float *img = x + (int64_t)b * h * w * c;
+        int32_t ssum = 0;
+        int k = 0, ky = 0, kx = 0, ci = 0;
+        for (int g = 0; g < kp / 16; ++g) {
+            uint32_t wv[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int u = 0; u < 16; ++u, ++k) {
+                if (k < K) {
+                    const int iy = oy * sh + ky * dh - pt, ix = ox * sw + kx * dw - pl;
+                    uint32_t byte;
+                    if (iy < 0 || iy >= h || ix < 0 || ix >= w) {  // zero-point border (axconv.py:185-189)
+                        byte = zpraw;
+                        ssum += q.zp;
+                    } else {
+                        const float e = __ldg(img + ((int64_t)iy * w + ix) * c + ci);
+                        int uo;
+                        const float uf = fmaf(e, q.inv, q.zpo);
+                        const float rr = rintf(uf);
+                        if (nearest && fabsf(uf - rr) < 0.49975f) {
+                            uo = min(max((int)rr, 0), 255);
+                        } else {
+                            nonfinite |= !(fabsf(e) <= 3.402823466e38f);
+                            uo = quant_any_u(q, e, nearest);
+                        }
+                        ssum += uo + lo;
+                        byte = (uint32_t)(uo + lo) & 0xFFu;
+                    }
+                    wv[u >> 2] |= byte << (8 * (u & 3));
+                    if (++ci == c) {
+                        ci = 0;
+                        if (++kx == kw) {
+                            kx = 0;
+                            ++ky;
+                        }
+                    }
+                }
+            }
+            reinterpret_cast<uint4 *>(rows + (int64_t)r * kp)[g] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        rowsum[r] = ssum;
+    }
+    if (__syncthreads_or(nonfinite) && threadIdx.x == 0 && d_flags) atomicOr(d_flags, AXB_FLAG_NONFINITE);
+}
+
 }  // namespace axb
 
 // ======================================================================== C ABI
@@ -498,6 +567,26 @@ int axb_im2col_pack(const uint8_t *d_codes, int64_t n, int64_t hp, int64_t wp, i
         d_codes, n, hp, wp, cs, (int)c, kh, kw, sh, sw, dh, dw, oh, ow, make_fastdiv((uint32_t)oh),
         make_fastdiv((uint32_t)ow), (int)kp, is_signed, d_rows, d_rowsum);
     return check_launch("im2col_pack");
+}
+
+int axb_quantize_im2col(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pl,
+                        int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t dh, int32_t dw, int64_t oh, int64_t ow,
+                        int64_t kp, const int32_t *d_range, axb_qparams *d_params, int is_signed, int round_mode,
+                        uint8_t *d_rows, int32_t *d_rowsum, int32_t *d_flags, void *stream) {
+    const int64_t rows = n * oh * ow;
+    if (rows == 0) return AXB_OK;
+    if (!d_params) return set_error(AXB_E_VALUE, "null parameter buffer");
+    if (kp % 16 || kp < kh * kw * c) return set_error(AXB_E_VALUE, "bad im2col row length");
+    if (rows >= (int64_t(1) << 32) || n * h * w * c >= (int64_t(1) << 40))
+        return set_error(AXB_E_VALUE, "quantize_im2col: tensor too large");
+    int64_t blocks = (rows + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    quantize_im2col_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(
+        d_x, (int)n, (int)h, (int)w, (int)c, pt, pl, kh, kw, sh, sw, dh, dw, (int)oh, (int)ow,
+        make_fastdiv((uint32_t)oh), make_fastdiv((uint32_t)ow), (int)kp, d_params, d_range, is_signed, round_mode,
+        d_rows, d_rowsum, d_flags);
+    return check_launch("quantize_im2col");
 }
 
 int axb_range_reset(int32_t *d_range, void *stream) {

@@ -118,29 +118,29 @@ class ConvLayer:
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self.launches = 0
         qflag = quant_flag if quant_flag is not None else out_flag
-        codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
-        pixsum = torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
-        if in_range_dev is not None:  # coefficients of the device range computed inside the quantize kernel
-            _lib.check(lib.axb_quantize_pad_range(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, in_range_dev,
-                                                  self.sgn, self.round, self.params[0].data_ptr(), codes.data_ptr(),
-                                                  pixsum.data_ptr(), qflag, stream))
-        else:
-            _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs,
-                                            self.params[0].data_ptr(), self.sgn, self.round, codes.data_ptr(),
-                                            pixsum.data_ptr(), qflag, stream))
-        self.launches += 1
         d = _lib.ConvDesc()
-        if self.kp:
-            rows = torch.empty(n * oh * ow * self.kp, dtype=torch.uint8, device=self.device)
-            rsum = torch.empty(n * oh * ow, dtype=torch.int32, device=self.device)
-            _lib.check(lib.axb_im2col_pack(codes.data_ptr(), n, hp_, wp_, self.cs, c, self.kh, self.kw,
-                                           g.strides[0], g.strides[1], g.dilations[0], g.dilations[1], oh, ow,
-                                           self.kp, self.sgn, rows.data_ptr(), rsum.data_ptr(), stream))
+        if self.kp:  # small-c layer: quantize + zp-pad + im2col in one pass into kp-byte code rows
+            codes = torch.empty(n * oh * ow * self.kp, dtype=torch.uint8, device=self.device)
+            pixsum = torch.empty(n * oh * ow, dtype=torch.int32, device=self.device)
+            _lib.check(lib.axb_quantize_im2col(x.data_ptr(), n, h, w, c, pt, pl, self.kh, self.kw, g.strides[0],
+                                               g.strides[1], g.dilations[0], g.dilations[1], oh, ow, self.kp,
+                                               in_range_dev, self.params[0].data_ptr(), self.sgn, self.round,
+                                               codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
             self.launches += 1
-            codes, pixsum = rows, rsum
             d.n, d.hp, d.wp, d.cs, d.c = n, oh, ow, self.kp, self.kh * self.kw * c
             d.kh = d.kw = d.sh = d.sw = d.dh = d.dw = 1
         else:
+            codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
+            pixsum = torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
+            if in_range_dev is not None:  # coefficients of the device range computed inside the quantize kernel
+                _lib.check(lib.axb_quantize_pad_range(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, in_range_dev,
+                                                      self.sgn, self.round, self.params[0].data_ptr(),
+                                                      codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
+            else:
+                _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs,
+                                                self.params[0].data_ptr(), self.sgn, self.round, codes.data_ptr(),
+                                                pixsum.data_ptr(), qflag, stream))
+            self.launches += 1
             d.n, d.hp, d.wp, d.cs, d.c = n, hp_, wp_, in_cs, c
             d.kh, d.kw = self.kh, self.kw
             d.sh, d.sw = g.strides

@@ -520,3 +520,59 @@ def test_graph_on_cifar_records_matches_images():
     bad[5, 0] = 11
     with pytest.raises(F.FormatError, match="label"):
         g.run(torch.from_numpy(bad).cuda())
+
+
+@pytest.mark.parametrize("mode", [O.SIGNED, O.UNSIGNED])
+def test_fused_quantize_im2col_equals_two_pass(mode):
+    """axb_quantize_im2col (one pass, fp32 -> code rows) == axb_quantize_pad + axb_im2col_pack,
+    rows and row sums, with host parameters and with in-kernel coefficients of a device range."""
+    torch = _torch()
+    from paper_2002_09481_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(5)
+    for (n, h, w, c, kh, kw, s, d, pads) in [(3, 17, 13, 3, 3, 3, 1, 1, (1, 1, 1, 1)), (2, 23, 23, 3, 7, 7, 2, 1, (3, 3, 3, 3)),
+                                              (4, 9, 11, 5, 3, 2, 2, 2, (0, 2, 1, 0)), (1, 8, 8, 1, 5, 5, 1, 1, (2, 2, 2, 2))]:
+        x = rng.uniform(-1.5, 2.5, (n, h, w, c)).astype(np.float32)
+        x[0, 0, 0, 0] = 0.5  # a few exact half-steps / ties
+        pt, pb, pl, pr = pads
+        hp, wp = h + pt + pb, w + pl + pr
+        oh, ow = (hp - ((kh - 1) * d + 1)) // s + 1, (wp - ((kw - 1) * d + 1)) // s + 1
+        cs = int(lib.axb_channel_stride(c))
+        kp = int(lib.axb_conv_im2col_kp(c, kh, kw))
+        xd = torch.from_numpy(x).cuda()
+        rngd = torch.tensor([np.float32(x.min()).view(np.int32), np.float32(x.max()).view(np.int32)], dtype=torch.int32,
+                            device="cuda")
+        rngd = torch.where(rngd >= 0, rngd, rngd ^ 0x7FFFFFFF)
+        sgn = int(mode == O.SIGNED)
+        for use_range in (False, True):
+            params = torch.zeros(2, _lib.QPARAMS_BYTES, dtype=torch.uint8, device="cuda")
+            if not use_range:
+                hpq = _lib.QParams()
+                _lib.check(lib.axb_coeffs_host(float(x.min()), float(x.max()), sgn, 0, hpq))
+                _lib.check(lib.axb_params_upload(hpq, params[0].data_ptr(), None))
+                _lib.check(lib.axb_params_upload(hpq, params[1].data_ptr(), None))
+            codes = torch.empty(n * hp * wp * cs, dtype=torch.uint8, device="cuda")
+            pix = torch.empty(n * hp * wp, dtype=torch.int32, device="cuda")
+            fl = torch.zeros(2, dtype=torch.int32, device="cuda")
+            r_ptr = rngd.data_ptr() if use_range else None
+            if use_range:
+                _lib.check(lib.axb_quantize_pad_range(xd.data_ptr(), n, h, w, c, pt, pb, pl, pr, cs, r_ptr, sgn, 0,
+                                                      params[0].data_ptr(), codes.data_ptr(), pix.data_ptr(),
+                                                      fl.data_ptr(), None))
+            else:
+                _lib.check(lib.axb_quantize_pad(xd.data_ptr(), n, h, w, c, pt, pb, pl, pr, cs, params[0].data_ptr(),
+                                                sgn, 0, codes.data_ptr(), pix.data_ptr(), fl.data_ptr(), None))
+            rows1 = torch.empty(n * oh * ow * kp, dtype=torch.uint8, device="cuda")
+            sum1 = torch.empty(n * oh * ow, dtype=torch.int32, device="cuda")
+            _lib.check(lib.axb_im2col_pack(codes.data_ptr(), n, hp, wp, cs, c, kh, kw, s, s, d, d, oh, ow, kp, sgn,
+                                           rows1.data_ptr(), sum1.data_ptr(), None))
+            rows2 = torch.empty_like(rows1)
+            sum2 = torch.empty_like(sum1)
+            _lib.check(lib.axb_quantize_im2col(xd.data_ptr(), n, h, w, c, pt, pl, kh, kw, s, s, d, d, oh, ow, kp,
+                                               r_ptr, params[1].data_ptr(), sgn, 0, rows2.data_ptr(),
+                                               sum2.data_ptr(), fl[1:].data_ptr(), None))
+            torch.cuda.synchronize()
+            assert torch.equal(rows1, rows2), (n, h, w, c, kh, kw, use_range)
+            assert torch.equal(sum1, sum2)
+            assert int(fl[1].item()) == 0
