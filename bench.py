@@ -230,6 +230,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layers-out", default="")
+    ap.add_argument("--no-autotune", action="store_true", help="use the cost model's kernel variants")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -285,9 +286,14 @@ def main():
     x_dev = torch.from_numpy(imgs).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    # warm-up (also prepares filters once: hoisted quantize_filters), then CUDA-graph capture
+    # warm-up (also prepares filters once: hoisted quantize_filters), per-layer kernel autotune on the
+    # first batch (outside the timed region; bit-identity of all variants checked), CUDA-graph capture
     for _ in range(args.warmup):
         ys = run_all(x_dev, check=True)
+    tuned = {} if args.no_autotune else graphs[0].autotune(x_dev)
+    for g in graphs[1:]:
+        if not args.no_autotune:
+            g.autotune(x_dev)
     torch.cuda.synchronize()
     launches = sum(g.launches for g in graphs)
     for g in graphs:
@@ -437,7 +443,8 @@ def main():
                    "parallelism": (f"dp{world} (candidate tables sharded round-robin)" if spec.get("sweep")
                                    else f"dp{world} (one range-batch per GPU)"),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "step": "one CUDA-graph replay of the whole graph (captured after warm-up)"},
+                   "step": "one CUDA-graph replay of the whole graph (captured after warm-up)",
+                   "kernel_variants": "autotuned per layer on the first batch" if tuned else "cost model"},
         "roofline": roofline,
         "e2e": {"value": round(e2e_gmacs, 2), "unit": "GMAC/s", "images_per_s": round(images / (e2e_total / 1e3), 2),
                 "h2d_bytes_per_step": int(x_hosts[0].numel() * x_hosts[0].element_size() * nets),
@@ -454,7 +461,8 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_rate(spec, macs_img, budget_s=args.cpu_budget)
     if args.layers_out:
-        rows = [{"node": k, "ms": round(v[0] / v[2], 4), "gmacs": round(v[1] / (v[0] / 1e3) / 1e9, 1),
+        rows = [{"node": k, "variant": tuned.get(k, "auto"), "ms": round(v[0] / v[2], 4),
+                 "gmacs": round(v[1] / (v[0] / 1e3) / 1e9, 1),
                  "frac": round(v[1] / (v[0] / 1e3) / peak_lookups, 4)} for k, v in layer_rows.items()]
         Path(args.layers_out).write_text(json.dumps(rows, indent=1))
     print(json.dumps(line), flush=True)

@@ -68,6 +68,7 @@ class _ConvPlan:
     out_shape: tuple = ()
     pads: tuple = ()
     layer: ConvLayer | None = None
+    ft_variant: int = 0         # ftable-kernel tile variant (0 = cost model; set by autotune)
 
 
 @dataclass
@@ -95,6 +96,7 @@ class GpuGraph:
         self.variant = int(variant)
         self.lib = _lib.load()
         self.labels = None  # device labels of the last record batch
+        self._tune = 0  # autotune repetitions per variant while > 0
         self._slot_sets = {}  # (input shape, dtype) -> captured CUDA-graph slots
         self._plan()
 
@@ -352,6 +354,21 @@ class GpuGraph:
             out = out.reshape(out.shape[0], 1, 1, out.shape[1])
         return out
 
+    def autotune(self, batch: torch.Tensor, reps: int = 3) -> dict:
+        """Pick each conv layer's ftable-kernel variant by timing every variant on the layer's
+        real input (one pass over ``batch``; like a cuDNN benchmark mode).  All variants must
+        produce identical bits -- checked here, on live data.  Returns {node id: variant name}."""
+        self._tune = max(1, int(reps))
+        try:
+            self.run(batch)
+        finally:
+            self._tune = 0
+        names = {}
+        for st in self.steps:
+            if st.kind == "conv" and st.plan.ft_variant:
+                names[st.node["id"]] = self.lib.axb_ft_variant_name(st.plan.ft_variant).decode()
+        return names
+
     def check_flags(self):
         self._check_flag_array(self.flags.cpu().numpy())
 
@@ -455,9 +472,28 @@ class GpuGraph:
         x = vals[self.t(p.x)]
         res = vals[self.t(p.residual)] if p.residual is not None else None
         prof = [] if self._profile is not None else None
-        out = p.layer.run(x, self.ranges[self.slot[self.t(p.x)]].data_ptr(), relu=p.relu, residual=res,
-                          out_range=out_range, out_flag=out_flag, quant_flag=self.flags[len(self.slot)].data_ptr(),
-                          sm_limit=self.sm_limit, variant=self.variant, profile=prof)
+        kw = dict(relu=p.relu, residual=res, out_range=out_range, out_flag=out_flag,
+                  quant_flag=self.flags[len(self.slot)].data_ptr(), sm_limit=self.sm_limit, variant=self.variant)
+        in_rng = self.ranges[self.slot[self.t(p.x)]].data_ptr()
+        if self._tune and p.layer.ftable is not None and not self.variant:
+            # re-running the layer is idempotent: same codes, same outputs, same range / flag bits
+            best, best_t, ref = 0, float("inf"), None
+            for v in range(1, self.lib.axb_ft_variant_count()):
+                evs = []
+                for _ in range(self._tune):
+                    pr = []
+                    y = p.layer.run(x, in_rng, ft_variant=v, profile=pr, **kw)
+                    evs.append(pr[0])
+                torch.cuda.synchronize(self.device)
+                t = sorted(a.elapsed_time(b) for a, b, *_ in evs)[len(evs) // 2]
+                if ref is None:
+                    ref = y
+                elif not torch.equal(ref.view(torch.int32), y.view(torch.int32)):
+                    raise _lib.AxbError(f"ftable variant {v} changed the bits of {p.node['id']!r}")
+                if t < best_t:
+                    best, best_t = v, t
+            p.ft_variant = best
+        out = p.layer.run(x, in_rng, profile=prof, ft_variant=p.ft_variant, **kw)
         if prof:
             self._profile.append((p.node["id"],) + prof[0])
         self.launches += p.layer.launches

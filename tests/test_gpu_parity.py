@@ -576,3 +576,21 @@ def test_fused_quantize_im2col_equals_two_pass(mode):
             assert torch.equal(rows1, rows2), (n, h, w, c, kh, kw, use_range)
             assert torch.equal(sum1, sum2)
             assert int(fl[1].item()) == 0
+
+
+def test_graph_autotune_keeps_bits():
+    """Per-layer kernel autotune (every ftable variant timed on live activations, bits compared
+    inside) leaves the logits bit-identical to the cost-model run and to the oracle graph."""
+    torch = _torch()
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.datasets import synthetic_cifar10
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    imgs, _ = synthetic_cifar10(64, seed=33)
+    g = GpuGraph(resnet.cifar_resnet(1, T.truncated_lut(T.Signedness.SIGNED, 2), seed=0))
+    x = torch.from_numpy(imgs).cuda()
+    want = g.run(x).cpu().numpy()
+    picks = g.autotune(x, reps=1)
+    assert len(picks) == 10 and all(v.startswith("ft") for v in picks.values()), picks
+    assert bits_equal(g.run(x).cpu().numpy(), want)
