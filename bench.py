@@ -291,9 +291,9 @@ def main():
     for _ in range(args.warmup):
         ys = run_all(x_dev, check=True)
     tuned = {} if args.no_autotune else graphs[0].autotune(x_dev)
-    for g in graphs[1:]:
-        if not args.no_autotune:
-            g.autotune(x_dev)
+    for g in graphs[1:]:  # same architecture (sweep candidates): same shapes -> same picks
+        if tuned:
+            g.copy_tuning(graphs[0])
     torch.cuda.synchronize()
     launches = sum(g.launches for g in graphs)
     for g in graphs:

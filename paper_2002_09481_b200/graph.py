@@ -41,6 +41,18 @@ _I32_MAX = 2**31 - 1
 _I32_MIN = -(2**31)
 
 
+_POOLS: dict = {}
+
+
+def _graph_pool(device):
+    """One CUDA-graph memory pool per device, shared by every captured step: captures free all
+    their intermediates, outputs are copied to static buffers, and replays never overlap."""
+    key = torch.device(device).index
+    if key not in _POOLS:
+        _POOLS[key] = torch.cuda.graph_pool_handle()
+    return _POOLS[key]
+
+
 def _geometry(attrs) -> ConvGeometry:
     pad = attrs.get("padding", "valid")
     if isinstance(pad, list):
@@ -369,6 +381,16 @@ class GpuGraph:
                 names[st.node["id"]] = self.lib.axb_ft_variant_name(st.plan.ft_variant).decode()
         return names
 
+    def copy_tuning(self, other: "GpuGraph") -> None:
+        """Adopt another graph's per-layer kernel choices (same architecture, e.g. the candidate
+        tables of a multiplier sweep: variants depend on shapes, not on table contents)."""
+        mine = [st.plan for st in self.steps if st.kind == "conv"]
+        theirs = [st.plan for st in other.steps if st.kind == "conv"]
+        if len(mine) != len(theirs):
+            raise ValueError("copy_tuning needs graphs of the same architecture")
+        for a, b in zip(mine, theirs):
+            a.ft_variant = b.ft_variant
+
     def check_flags(self):
         self._check_flag_array(self.flags.cpu().numpy())
 
@@ -387,11 +409,15 @@ class GpuGraph:
         with torch.cuda.stream(side):
             for _ in range(slots):
                 x = torch.zeros(in_shape, dtype=dtype, device=self.device)
-                self.run(x, check=False)  # warm-up: filter prep, shared-memory attributes, allocator
+                y0 = self.run(x, check=False)  # warm-up: filter prep, shared-memory attributes, allocator
+                # the step's results land in static buffers outside the graph pool, so every
+                # capture on this device can share one pool (replays are stream-ordered)
+                y = torch.empty_like(y0)
+                fl = torch.empty_like(self.flags)
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=side):
-                    y = self.run(x, check=False)
-                    fl = self.flags.clone()
+                with torch.cuda.graph(g, stream=side, pool=_graph_pool(self.device)):
+                    y.copy_(self.run(x, check=False))
+                    fl.copy_(self.flags)
                 self._slots.append({"graph": g, "x": x, "y": y, "flags": fl})
         stream.wait_stream(side)
         torch.cuda.synchronize(self.device)
