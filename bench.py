@@ -81,6 +81,12 @@ def workload_spec(name: str, lut_kind: str):
     raise SystemExit(f"unknown workload {name}")
 
 
+def lib_variant_name(v: int) -> str:
+    from paper_2002_09481_b200 import _lib
+
+    return _lib.load().axb_ft_variant_name(int(v)).decode() if v else "auto"
+
+
 def sweep_luts():
     """Config 4's 32 candidate multipliers."""
     from paper_2002_09481_b200 import types as T
@@ -231,6 +237,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layers-out", default="")
     ap.add_argument("--no-autotune", action="store_true", help="use the cost model's kernel variants")
+    ap.add_argument("--tuned-out", default="", help="write the autotuned per-layer variants (json)")
+    ap.add_argument("--tuned-from", default="", help="use per-layer variants from a --tuned-out file")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -290,7 +298,13 @@ def main():
     # first batch (outside the timed region; bit-identity of all variants checked), CUDA-graph capture
     for _ in range(args.warmup):
         ys = run_all(x_dev, check=True)
-    tuned = {} if args.no_autotune else graphs[0].autotune(x_dev)
+    if args.tuned_from:  # replay an earlier run's picks (e.g. under ncu, whose replays distort timing)
+        graphs[0].set_tuning(json.loads(Path(args.tuned_from).read_text()))
+        tuned = {"from": args.tuned_from}
+    else:
+        tuned = {} if args.no_autotune else graphs[0].autotune(x_dev)
+        if tuned and args.tuned_out:
+            Path(args.tuned_out).write_text(json.dumps(graphs[0].tuning()))
     for g in graphs[1:]:  # same architecture (sweep candidates): same shapes -> same picks
         if tuned:
             g.copy_tuning(graphs[0])
@@ -461,7 +475,8 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_rate(spec, macs_img, budget_s=args.cpu_budget)
     if args.layers_out:
-        rows = [{"node": k, "variant": tuned.get(k, "auto"), "ms": round(v[0] / v[2], 4),
+        picks = graphs[0].tuning()
+        rows = [{"node": k, "variant": lib_variant_name(picks.get(k, 0)), "ms": round(v[0] / v[2], 4),
                  "gmacs": round(v[1] / (v[0] / 1e3) / 1e9, 1),
                  "frac": round(v[1] / (v[0] / 1e3) / peak_lookups, 4)} for k, v in layer_rows.items()]
         Path(args.layers_out).write_text(json.dumps(rows, indent=1))

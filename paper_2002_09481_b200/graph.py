@@ -381,6 +381,15 @@ class GpuGraph:
                 names[st.node["id"]] = self.lib.axb_ft_variant_name(st.plan.ft_variant).decode()
         return names
 
+    def tuning(self) -> dict:
+        """{conv node id: ftable variant index} (0 = cost model)."""
+        return {st.node["id"]: st.plan.ft_variant for st in self.steps if st.kind == "conv"}
+
+    def set_tuning(self, picks: dict) -> None:
+        for st in self.steps:
+            if st.kind == "conv" and st.node["id"] in picks:
+                st.plan.ft_variant = int(picks[st.node["id"]])
+
     def copy_tuning(self, other: "GpuGraph") -> None:
         """Adopt another graph's per-layer kernel choices (same architecture, e.g. the candidate
         tables of a multiplier sweep: variants depend on shapes, not on table contents)."""
