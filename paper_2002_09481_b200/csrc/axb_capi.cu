@@ -259,6 +259,7 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
     axb_qparams *dp = nullptr;
     uint8_t *fcodes = nullptr;
     int64_t *fsum = nullptr;
+    uint32_t *ftable = nullptr;
     int rc = AXB_OK;
     auto fail = [&](int code, const char *msg) {
         if (rc == AXB_OK) rc = set_error(code, msg);
@@ -299,6 +300,19 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
             d.n = n; d.hp = hp; d.wp = wp; d.cs = cs; d.c = c;
             d.kh = (int32_t)kh; d.kw = (int32_t)kw; d.sh = sh; d.sw = sw; d.dh = dh; d.dw = dw;
         }
+        // Large calls: build the filter-specialised product table for this call (512 B per weight,
+        // one HBM-bound pass) and run the packed-pair kernel; small calls keep the LUT kernel.
+        const int64_t ft_bytes = axb_ftable_bytes(kpad, coutp);
+        if (n * oh * ow >= 4096 && kpad <= 32768 && fkh * fkw <= 256 && ft_bytes > 0 &&
+            ft_bytes <= (int64_t(1) << 30)) {
+            if (cudaMallocAsync(&ftable, ft_bytes, s) != cudaSuccess) {
+                cudaGetLastError();  // no room: fall back to the LUT kernel
+                ftable = nullptr;
+            } else {
+                rc = axb_ftable_prepare(fcodes, fkh, fkw, fc, fcs, cout, lut, ftable, s);
+                d.ftable = ftable;
+            }
+        }
         d.oh = oh; d.ow = ow;
         d.fcodes = fcodes; d.fsum = fsum; d.cout = cout; d.coutp = coutp; d.kpad = kpad;
         d.in_params = dp; d.f_params = dp + 1;
@@ -306,7 +320,7 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
         d.out = d_out;
         d.acc_out = d_acc_out;
         d.flags = flags + 1;
-        rc = axb_conv2d_lut(&d, lut, s);
+        if (!rc) rc = axb_conv2d_lut(&d, lut, s);
     }
     if (!rc) {  // error precedence as in axconv.py: filters (:287), then inputs (:294)
         int32_t hf[2] = {0, 0};
@@ -317,6 +331,7 @@ int axb_axconv2d(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, c
         else if (hf[1] & AXB_FLAG_NONFINITE) fail(AXB_E_VALUE, "cannot quantize non-finite values");
         else if (hf[1] & AXB_FLAG_PSUM_OVF) fail(AXB_E_OVERFLOW, "patch length too large for 32-bit code sums");
     }
+    if (ftable) cudaFreeAsync(ftable, s);
     cudaFreeAsync(codes, s);
     cudaFreeAsync(pixsum, s);
     if (rows) cudaFreeAsync(rows, s);
