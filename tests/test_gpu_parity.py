@@ -594,3 +594,21 @@ def test_graph_autotune_keeps_bits():
     picks = g.autotune(x, reps=1)
     assert len(picks) == 10 and all(v.startswith("ft") for v in picks.values()), picks
     assert bits_equal(g.run(x).cpu().numpy(), want)
+
+
+def test_operator_api_large_call_uses_ftable_bit_exact():
+    """torch_axconv2d on the 1000-image first layer (test_axconv.py:225-237): large calls build the
+    filter-specialised table per call; output sha == the reference's."""
+    torch = _torch()
+    from paper_2002_09481_b200 import _lib
+    from paper_2002_09481_b200.axconv import torch_axconv2d
+    from paper_2002_09481_b200.types import ConvGeometry
+
+    g = load_golden("kat")
+    rng = np.random.default_rng(8)
+    xs = rng.uniform(0, 1, (1000, 32, 32, 3)).astype(np.float32)
+    fs = rng.normal(0, 0.4, (3, 3, 3, 16)).astype(np.float32)
+    y = torch_axconv2d(torch.from_numpy(xs).cuda(), torch.from_numpy(fs).cuda(), (0.0, 1.0), (-2.0, 2.0),
+                       _lut(O.exact_lut(O.SIGNED), O.SIGNED), ConvGeometry(padding="same"))
+    assert _lib.last_kernel().startswith("ft"), _lib.last_kernel()
+    assert hashlib.sha256(y.cpu().numpy().tobytes()).digest() == g["scale_sha"].tobytes()
