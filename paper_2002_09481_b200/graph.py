@@ -461,9 +461,11 @@ class GpuGraph:
         outs = host_outputs if host_outputs is not None else [
             torch.empty(tuple(self._slots[0]["y"].shape), dtype=torch.float32).pin_memory() for _ in host_batches]
         fl_host = torch.empty((len(host_batches), self.flags.numel()), dtype=torch.int32).pin_memory()
+        d2h = torch.cuda.Stream(self.device)
         h2d_done = [torch.cuda.Event() for _ in range(nsl)]
-        slot_free = [torch.cuda.Event() for _ in range(nsl)]
-        for e in slot_free:
+        slot_free = [torch.cuda.Event() for _ in range(nsl)]   # replay finished: input / output readable
+        out_free = [torch.cuda.Event() for _ in range(nsl)]    # D2H of the slot's output finished
+        for e in slot_free + out_free:
             e.record(comp)
 
         def h2d(i):
@@ -481,10 +483,15 @@ class GpuGraph:
                 h2d(i + 1)
             if before_step is not None:
                 before_step()  # e.g. the benchmark's L2 flush, on the compute stream
+            comp.wait_event(out_free[i % nsl])  # the slot's previous output has left the device
             sl["graph"].replay()
-            outs[i].copy_(sl["y"], non_blocking=True)
-            fl_host[i].copy_(sl["flags"], non_blocking=True)
             slot_free[i % nsl].record(comp)
+            d2h.wait_event(slot_free[i % nsl])  # results come back on their own stream, overlapping step i+1
+            with torch.cuda.stream(d2h):
+                outs[i].copy_(sl["y"], non_blocking=True)
+                fl_host[i].copy_(sl["flags"], non_blocking=True)
+            out_free[i % nsl].record(d2h)
+        comp.wait_stream(d2h)
         comp.synchronize()
         for i in range(len(host_batches)):
             self._check_flag_array(fl_host[i].numpy())
