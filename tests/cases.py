@@ -76,3 +76,24 @@ def oracle_conv(case, engine="gemm", return_acc=False):
         return O.axconv2d(case["x"], case["f"], case["in_range"], case["f_range"], case["lut"],
                           case["mode"], return_acc=True, **kw)
     return fn(case["x"], case["f"], case["in_range"], case["f_range"], case["lut"], case["mode"], **kw)
+
+
+def model_graph_spec():
+    """Deterministic small float graph: conv-relu-conv(stride 2)+proj add-relu-avgpool-1x1 conv."""
+    rng = np.random.default_rng(99)
+    f = lambda *s: (rng.standard_normal(s) * 0.3).astype(np.float32)  # noqa: E731
+    return [
+        ("in", "Input", [], {"shape": [12, 12, 3]}),
+        ("c1", "Conv2D", ["in"], {"filters": f(3, 3, 3, 8), "bias": f(8), "strides": [1, 1], "dilations": [1, 1],
+                                  "padding": "same"}),
+        ("r1", "ReLU", ["c1"], {}),
+        ("c2", "Conv2D", ["r1"], {"filters": f(3, 3, 8, 16), "bias": f(16), "strides": [2, 2], "dilations": [1, 1],
+                                  "padding": "same"}),
+        ("p2", "Conv2D", ["r1"], {"filters": f(1, 1, 8, 16), "strides": [2, 2], "dilations": [1, 1],
+                                  "padding": "valid"}),
+        ("a2", "Add", ["c2", "p2"], {}),
+        ("r2", "ReLU", ["a2"], {}),
+        ("gp", "AvgPool", ["r2"], {"pool": [6, 6], "strides": [6, 6], "padding": "valid"}),
+        ("fc", "Conv2D", ["gp"], {"filters": f(1, 1, 16, 5), "bias": f(5), "strides": [1, 1], "dilations": [1, 1],
+                                  "padding": "valid"}),
+    ]

@@ -272,7 +272,27 @@ def make_formats() -> dict:
         out["cifar_labels"] = batch.labels
         rep = make_report(0.25, 1.5, 0.75, 0.5, 123456, {"conv1": 0.4, "conv2": 0.35})
         out["report_csv"] = np.frombuffer(report_csv(rep).encode(), np.uint8)
+        # a small float model -> transform -> save_model (graph.py:107-141, formats.py:298-339), and its
+        # logits through the reference executor
+        from axemu import LayerGraph, Node, NodeKind, run, save_model, transform
+
+        g = LayerGraph(model_graph_reference(Node, NodeKind))
+        tg, rep = transform(g, truncated_lut(Signedness.SIGNED, 2))
+        out["model_transform_report"] = np.array([rep.replaced_count, rep.inserted_min_max])
+        save_model(tg, td / "ax.json")
+        out["model_json"] = np.frombuffer((td / "ax.json").read_bytes(), np.uint8)
+        out["model_weights"] = np.frombuffer((td / "ax.weights.bin").read_bytes(), np.uint8)
+        out["model_axm_sha"] = np.frombuffer(bytes.fromhex(hashlib.sha256((td / "ax.axm").read_bytes()).hexdigest()),
+                                             np.uint8)
+        x = np.random.default_rng(17).uniform(0, 1, (4, 12, 12, 3)).astype(np.float32)
+        out["model_input"] = x
+        out["model_logits"] = run(tg, Tensor4(x), engine="gemm").data
     return out
+
+
+def model_graph_reference(Node, NodeKind):
+    kinds = {k.value: k for k in NodeKind}
+    return [Node(i, kinds[k], list(ins), dict(a)) for i, k, ins, a in my_cases.model_graph_spec()]
 
 
 def main():

@@ -612,3 +612,21 @@ def test_operator_api_large_call_uses_ftable_bit_exact():
                        _lut(O.exact_lut(O.SIGNED), O.SIGNED), ConvGeometry(padding="same"))
     assert _lib.last_kernel().startswith("ft"), _lib.last_kernel()
     assert hashlib.sha256(y.cpu().numpy().tobytes()).digest() == g["scale_sha"].tobytes()
+
+
+def test_reference_model_file_runs_bit_exact(tmp_path):
+    """A model file written by the reference (transform + save_model) loads with model.load_model
+    and runs on the GPU executor with the reference executor's logits, bit for bit."""
+    torch = _torch()
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.formats import save_lut
+    from paper_2002_09481_b200.graph import GpuGraph
+    from paper_2002_09481_b200.model import load_model
+
+    g = load_golden("formats")
+    (tmp_path / "ax.json").write_bytes(g["model_json"].tobytes())
+    (tmp_path / "ax.weights.bin").write_bytes(g["model_weights"].tobytes())
+    save_lut(T.truncated_lut(T.Signedness.SIGNED, 2), tmp_path / "ax.axm")
+    nodes = load_model(tmp_path / "ax.json")
+    y = GpuGraph(nodes).run(torch.from_numpy(g["model_input"]).cuda()).cpu().numpy()
+    assert bits_equal(y, g["model_logits"])
