@@ -146,6 +146,12 @@ __device__ __forceinline__ void bulk_g2s_multicast(void *dst, const void *src, u
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
         : "memory");
 }
+// order this thread's generic-proxy shared-memory accesses before later async-proxy (TMA)
+// accesses to the same memory: a consumer executes it before releasing a stage that a TMA
+// bulk copy will overwrite (write-after-read across proxies)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }

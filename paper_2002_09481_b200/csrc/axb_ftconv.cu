@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
                         }
                     }
                 }
+                fence_proxy_async_smem();  // this lane's LDS reads of the slot before the TMA refill
                 __syncwarp();
                 if constexpr (CL == 1) {
                     if (lane == 0) mbar_arrive(empty + slot);

@@ -531,7 +531,10 @@ class GpuGraph:
                 if ref is None:
                     ref = y
                 elif not torch.equal(ref.view(torch.int32), y.view(torch.int32)):
-                    raise _lib.AxbError(f"ftable variant {v} changed the bits of {p.node['id']!r}")
+                    bad = (ref.view(torch.int32) != y.view(torch.int32)).reshape(-1).nonzero()
+                    raise _lib.AxbError(f"ftable variant {v} changed the bits of {p.node['id']!r}: {bad.numel()} of "
+                                        f"{y.numel()} outputs, first flat indices {bad[:4, 0].tolist()}, shape "
+                                        f"{tuple(y.shape)}")
                 if t < best_t:
                     best, best_t = v, t
             p.ft_variant = best

@@ -630,3 +630,20 @@ def test_reference_model_file_runs_bit_exact(tmp_path):
     nodes = load_model(tmp_path / "ax.json")
     y = GpuGraph(nodes).run(torch.from_numpy(g["model_input"]).cuda()).cpu().numpy()
     assert bits_equal(y, g["model_logits"])
+
+
+def test_r50_autotune_all_variants_agree():
+    """Regression for a write-after-read race between LDS reads of a ring stage and the TMA refill
+    (fixed with fence.proxy.async before the release): autotune compares every ftable variant's
+    bits on every ResNet-50 layer at batch 128, twice."""
+    torch = _torch()
+    from paper_2002_09481_b200 import datasets, resnet
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    g = GpuGraph(resnet.resnet50(T.truncated_lut(T.Signedness.SIGNED, 2), seed=0))
+    x = torch.from_numpy(datasets.uniform_images(128, 224, seed=3)).cuda()
+    want = g.run(x).clone()
+    for _ in range(2):
+        g.autotune(x, reps=1)
+        assert torch.equal(g.run(x).view(torch.int32), want.view(torch.int32))
