@@ -471,70 +471,106 @@ __global__ void __launch_bounds__(256) im2col_pack_kernel(const uint8_t *__restr
 }
 
 // ---------------------------------------------------------------- fused quantize + im2col (small-c layers)
-// One thread per output row: quantizes the kh*kw*c fp32 inputs of its window straight into
-// the kp-byte code row (zero-point code for padding taps, raw 0 beyond K) and writes the row
-// sum S_p -- the codes tensor of quantize_pad is never materialised.  Same per-element
-// arithmetic as quantize_pad16_kernel (fp32 estimate, exact fallback near ties / non-finite).
-__global__ void __launch_bounds__(256) quantize_im2col_kernel(
+// A block owns a QT_H x QT_W tile of output pixels of one image: it quantizes the input patch
+// those windows cover ONCE into shared memory (coalesced fp32 loads along the NHWC rows, the
+// zero-point code outside the image, axconv.py:185-189), then each thread gathers its window's
+// kh*kw*c codes into a kp-byte row (raw 0 beyond K) and writes the row sum S_p (axconv.py:193).
+// Same per-element arithmetic as quantize_pad16_kernel (fp32 estimate, exact fallback).
+constexpr int QT_H = 8, QT_W = 32;
+constexpr int kQiPatchMax = 12288;  // patch codes per block (e.g. 7x7 stride-2 stem: 21 x 69 x 3 = 4,347)
+constexpr int kMaxIm2colK = 1024;   // window elements kh*kw*c (K of the small-c layer)
+
+__host__ __device__ inline int qi_patch(int extent_out, int s, int k, int d) { return (extent_out - 1) * s + (k - 1) * d + 1; }
+
+__global__ void __launch_bounds__(QT_H *QT_W) quantize_im2col_kernel(
     const float *__restrict__ x, int n, int h, int w, int c, int pt, int pl, int kh, int kw, int sh, int sw, int dh,
-    int dw, int oh, int ow, FastDiv fd_oh, FastDiv fd_ow, int kp, axb_qparams *prm, const int32_t *d_range,
+    int dw, int oh, int ow, int tiles_y, int tiles_x, int kp, FastDiv fd_c, FastDiv fd_prow, axb_qparams *prm,
+    const int32_t *d_range,
     int is_signed, int round_mode, uint8_t *__restrict__ rows, int32_t *__restrict__ rowsum, int32_t *d_flags) {
     __shared__ QuantCtx q;
+    __shared__ uint8_t patch[kQiPatchMax];
+    __shared__ int16_t koff[kMaxIm2colK];  // patch offset of window element k = (ky, kx, ci)
     if (d_range)
         quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
     else
         quant_ctx_load(q, prm, is_signed);
     const bool nearest = round_mode != AXB_ROUND_TOWARD_ZERO;
     const int lo = q.lo;
-    const uint32_t zpraw = (uint32_t)(q.zp & 0xFF);
+    const int PH = qi_patch(QT_H, sh, kh, dh), PW = qi_patch(QT_W, sw, kw, dw);
+    const int prow = PW * c;  // codes per patch row
     const int K = kh * kw * c;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const int t = k / c, ci = k - t * c;
+        koff[k] = (int16_t)((t / kw) * dh * prow + (t % kw) * dw * c + ci);
+    }
     int nonfinite = 0;
-    const uint32_t total = (uint32_t)n * (uint32_t)oh * (uint32_t)ow;
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < total; r += gridDim.x * blockDim.x) {
-        const uint32_t t = fdiv(r, fd_ow);
-        const int ox = (int)(r - t * (uint32_t)ow);
-        const uint32_t b = fdiv(t, fd_oh);
-        const int oy = (int)(t - b * (uint32_t)oh);
+    const int tid = threadIdx.x;
+    for (int blk = blockIdx.x; blk < n * tiles_y * tiles_x; blk += gridDim.x) {
+        const int b = blk / (tiles_y * tiles_x);
+        const int t = blk - b * tiles_y * tiles_x;
+        const int oy0 = (t / tiles_x) * QT_H, ox0 = (t % tiles_x) * QT_W;
+        const int iy0 = oy0 * sh - pt, ix0 = ox0 * sw - pl;
         const float *img = x + (int64_t)b * h * w * c;
-        int32_t ssum = 0;
-        int k = 0, ky = 0, kx = 0, ci = 0;
-        for (int g = 0; g < kp / 16; ++g) {
-            uint32_t wv[4] = {0, 0, 0, 0};
+        __syncthreads();  // previous tile's gathers are done with the patch (and koff is written)
+        // the patch, flattened: 4 independent loads in flight per thread per pass
+        const int total = PH * prow;
+        for (int e0 = tid; e0 < total; e0 += 4 * QT_H * QT_W) {
+            float v[4];
+            bool in[4];
 #pragma unroll
-            for (int u = 0; u < 16; ++u, ++k) {
-                if (k < K) {
-                    const int iy = oy * sh + ky * dh - pt, ix = ox * sw + kx * dw - pl;
-                    uint32_t byte;
-                    if (iy < 0 || iy >= h || ix < 0 || ix >= w) {  // zero-point border (axconv.py:185-189)
-                        byte = zpraw;
-                        ssum += q.zp;
-                    } else {
-                        const float e = __ldg(img + ((int64_t)iy * w + ix) * c + ci);
-                        int uo;
-                        const float uf = fmaf(e, q.inv, q.zpo);
-                        const float rr = rintf(uf);
-                        if (nearest && fabsf(uf - rr) < 0.49975f) {
-                            uo = min(max((int)rr, 0), 255);
-                        } else {
-                            nonfinite |= !(fabsf(e) <= 3.402823466e38f);
-                            uo = quant_any_u(q, e, nearest);
-                        }
-                        ssum += uo + lo;
-                        byte = (uint32_t)(uo + lo) & 0xFFu;
-                    }
-                    wv[u >> 2] |= byte << (8 * (u & 3));
-                    if (++ci == c) {
-                        ci = 0;
-                        if (++kx == kw) {
-                            kx = 0;
-                            ++ky;
-                        }
-                    }
-                }
+            for (int j = 0; j < 4; ++j) {
+                const int e = e0 + j * QT_H * QT_W;
+                const uint32_t py = fdiv((uint32_t)e, fd_prow);
+                const int r = e - (int)py * prow;
+                const int iy = iy0 + (int)py, ix = ix0 + (int)fdiv((uint32_t)r, fd_c);
+                in[j] = e < total && iy >= 0 && iy < h && ix >= 0 && ix < w;
+                v[j] = in[j] ? __ldg(img + ((int64_t)iy * w + ix0) * c + r) : 0.0f;
             }
-            reinterpret_cast<uint4 *>(rows + (int64_t)r * kp)[g] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int e = e0 + j * QT_H * QT_W;
+                if (e >= total) break;
+                int code = q.zp;  // zero-point border
+                if (in[j]) {
+                    const float uf = fmaf(v[j], q.inv, q.zpo);
+                    const float rr = rintf(uf);
+                    int uo;
+                    if (nearest && fabsf(uf - rr) < 0.49975f) {
+                        uo = min(max((int)rr, 0), 255);
+                    } else {
+                        nonfinite |= !(fabsf(v[j]) <= 3.402823466e38f);
+                        uo = quant_any_u(q, v[j], nearest);
+                    }
+                    code = uo + lo;
+                }
+                patch[e] = (uint8_t)(code & 0xFF);
+            }
         }
-        rowsum[r] = ssum;
+        __syncthreads();
+        const int ty = tid / QT_W, tx = tid % QT_W;
+        const int oy = oy0 + ty, ox = ox0 + tx;
+        if (oy < oh && ox < ow) {
+            const uint8_t *base = patch + (ty * sh) * prow + (tx * sw) * c;
+            const int64_t r = ((int64_t)b * oh + oy) * ow + ox;
+            int32_t ssum = 0;
+            for (int g = 0; g < kp / 16; ++g) {
+                uint32_t wv[4];
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4) {
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = g * 16 + v4 * 4 + u;
+                        if (k < K) word |= (uint32_t)base[koff[k]] << (8 * u);
+                    }
+                    wv[v4] = word;
+                    ssum = is_signed ? __dp4a((int)word, 0x01010101, ssum)  // junk bytes are 0
+                                     : (int32_t)__dp4a(word, 0x01010101u, (uint32_t)ssum);
+                }
+                reinterpret_cast<uint4 *>(rows + r * kp)[g] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+            rowsum[r] = ssum;
+        }
     }
     if (__syncthreads_or(nonfinite) && threadIdx.x == 0 && d_flags) atomicOr(d_flags, AXB_FLAG_NONFINITE);
 }
@@ -569,6 +605,11 @@ int axb_im2col_pack(const uint8_t *d_codes, int64_t n, int64_t hp, int64_t wp, i
     return check_launch("im2col_pack");
 }
 
+static int quantize_pad_launch(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,
+                               int32_t pl, int32_t pr, int64_t cs, axb_qparams *d_params, const int32_t *d_range,
+                               int is_signed, int round_mode, uint8_t *d_codes, int32_t *d_pixsum, int32_t *d_flags,
+                               void *stream);
+
 int axb_quantize_im2col(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pl,
                         int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t dh, int32_t dw, int64_t oh, int64_t ow,
                         int64_t kp, const int32_t *d_range, axb_qparams *d_params, int is_signed, int round_mode,
@@ -579,13 +620,39 @@ int axb_quantize_im2col(const float *d_x, int64_t n, int64_t h, int64_t w, int64
     if (kp % 16 || kp < kh * kw * c) return set_error(AXB_E_VALUE, "bad im2col row length");
     if (rows >= (int64_t(1) << 32) || n * h * w * c >= (int64_t(1) << 40))
         return set_error(AXB_E_VALUE, "quantize_im2col: tensor too large");
-    int64_t blocks = (rows + 255) / 256;
-    const int64_t cap = (int64_t)sm_count() * 16;
+    if ((int64_t)qi_patch(QT_H, sh, kh, dh) * qi_patch(QT_W, sw, kw, dw) * c > kQiPatchMax ||
+        (int64_t)kh * kw * c > kMaxIm2colK) {
+        // window patch too large for the tiled kernel: quantize into a zp-padded code tensor, then gather
+        cudaStream_t st = (cudaStream_t)stream;
+        const int64_t need_h = (oh - 1) * sh + (kh - 1) * dh + 1, need_w = (ow - 1) * sw + (kw - 1) * dw + 1;
+        const int64_t pb = need_h - h - pt > 0 ? need_h - h - pt : 0, pr = need_w - w - pl > 0 ? need_w - w - pl : 0;
+        const int64_t hp = h + pt + pb, wp = w + pl + pr;
+        const int64_t cs = axb_channel_stride(c);
+        uint8_t *codes = nullptr;
+        int32_t *pix = nullptr;
+        if (cudaMallocAsync(&codes, n * hp * wp * cs, st) != cudaSuccess ||
+            cudaMallocAsync(&pix, n * hp * wp * 4, st) != cudaSuccess) {
+            if (codes) cudaFreeAsync(codes, st);
+            return set_error(AXB_E_CUDA, "quantize_im2col: scratch allocation failed");
+        }
+        int rc = quantize_pad_launch(d_x, n, h, w, c, pt, (int32_t)pb, pl, (int32_t)pr, cs, d_params, d_range,
+                                     is_signed, round_mode, codes, pix, d_flags, stream);
+        if (!rc)
+            rc = axb_im2col_pack(codes, n, hp, wp, cs, c, kh, kw, sh, sw, dh, dw, oh, ow, kp, is_signed, d_rows,
+                                 d_rowsum, stream);
+        cudaFreeAsync(codes, st);
+        cudaFreeAsync(pix, st);
+        return rc;
+    }
+    const int tiles_y = (int)((oh + QT_H - 1) / QT_H), tiles_x = (int)((ow + QT_W - 1) / QT_W);
+    int64_t blocks = n * tiles_y * tiles_x;
+    const int64_t cap = (int64_t)sm_count() * 8;
     if (blocks > cap) blocks = cap;
-    quantize_im2col_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(
-        d_x, (int)n, (int)h, (int)w, (int)c, pt, pl, kh, kw, sh, sw, dh, dw, (int)oh, (int)ow,
-        make_fastdiv((uint32_t)oh), make_fastdiv((uint32_t)ow), (int)kp, d_params, d_range, is_signed, round_mode,
-        d_rows, d_rowsum, d_flags);
+    quantize_im2col_kernel<<<(int)blocks, QT_H * QT_W, 0, (cudaStream_t)stream>>>(
+        d_x, (int)n, (int)h, (int)w, (int)c, pt, pl, kh, kw, sh, sw, dh, dw, (int)oh, (int)ow, tiles_y, tiles_x,
+        (int)kp, make_fastdiv((uint32_t)c),
+        make_fastdiv((uint32_t)(qi_patch(QT_W, sw, kw, dw) * c)), d_params, d_range, is_signed, round_mode, d_rows,
+        d_rowsum, d_flags);
     return check_launch("quantize_im2col");
 }
 

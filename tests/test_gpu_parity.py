@@ -532,7 +532,9 @@ def test_fused_quantize_im2col_equals_two_pass(mode):
     lib = _lib.load()
     rng = np.random.default_rng(5)
     for (n, h, w, c, kh, kw, s, d, pads) in [(3, 17, 13, 3, 3, 3, 1, 1, (1, 1, 1, 1)), (2, 23, 23, 3, 7, 7, 2, 1, (3, 3, 3, 3)),
-                                              (4, 9, 11, 5, 3, 2, 2, 2, (0, 2, 1, 0)), (1, 8, 8, 1, 5, 5, 1, 1, (2, 2, 2, 2))]:
+                                              (4, 9, 11, 5, 3, 2, 2, 2, (0, 2, 1, 0)), (1, 8, 8, 1, 5, 5, 1, 1, (2, 2, 2, 2)),
+                                              (2, 40, 37, 13, 7, 7, 2, 2, (6, 6, 6, 6)),  # patch > smem: two-pass path
+                                              (3, 70, 66, 3, 3, 3, 1, 1, (1, 1, 1, 1))]:  # several tiles per image
         x = rng.uniform(-1.5, 2.5, (n, h, w, c)).astype(np.float32)
         x[0, 0, 0, 0] = 0.5  # a few exact half-steps / ties
         pt, pb, pl, pr = pads
