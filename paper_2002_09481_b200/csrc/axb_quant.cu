@@ -293,6 +293,33 @@ __global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__rest
                                                              uint8_t *__restrict__ codes,
                                                              int32_t *__restrict__ pixsum, int32_t *d_flags) {
     __shared__ QuantCtx q;
+    const int c = 16 * C16;
+    const uint32_t npix = (uint32_t)n * (uint32_t)hp * (uint32_t)wp;
+    constexpr int PER = C16 <= 32 ? C16 : 32;  // lanes per pixel in the segmented sum
+    const uint32_t total = npix * (uint32_t)C16;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t bound = (total + 31u) & ~31u;
+    // chunk i -> (pixel p, 16-channel group j); its 16 inputs (false: zero-point border, axconv.py:185-189)
+    auto fetch = [&](uint32_t i, float (&e)[16]) -> bool {
+        const uint32_t p = i / C16, j = i % C16;
+        const uint32_t t = fdiv(p, fd_wp);
+        const int xw = (int)(p - t * (uint32_t)wp);
+        const uint32_t b = fdiv(t, fd_hp);
+        const int yh = (int)(t - b * (uint32_t)hp);
+        const int iy = yh - pt, ix = xw - pl;
+        if (iy < 0 || iy >= h || ix < 0 || ix >= w) return false;
+        const float4 *src = reinterpret_cast<const float4 *>(x + (((int64_t)b * h + iy) * w + ix) * c + j * 16);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float4 f = __ldg(src + v);
+            e[4 * v] = f.x; e[4 * v + 1] = f.y; e[4 * v + 2] = f.z; e[4 * v + 3] = f.w;
+        }
+        return true;
+    };
+    // the first chunk's loads are in flight while the prologue computes the coefficients
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    float e[16];
+    bool inside = i < total && fetch(i, e);
     if (d_range)
         quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
     else
@@ -303,37 +330,16 @@ __global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__rest
     const uint32_t flip = is_signed ? 0x80808080u : 0u;  // raw byte of code lo+u = (u + lo) & 0xFF
     const uint32_t zpw = (uint32_t)(q.zp & 0xFF) * 0x01010101u;
     const int zsum = 16 * q.zp;
-    const int c = 16 * C16;
     int nonfinite = 0;
-    const uint32_t npix = (uint32_t)n * (uint32_t)hp * (uint32_t)wp;
-    constexpr int PER = C16 <= 32 ? C16 : 32;  // lanes per pixel in the segmented sum
-    const uint32_t total = npix * (uint32_t)C16;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t bound = (total + 31u) & ~31u;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < bound; i += stride) {
+    for (; i < bound; i += stride) {
         int32_t s = 0;
-        uint32_t p = 0, j = 0;
+        const uint32_t p = i / C16, j = i % C16;
         if (i < total) {
-            p = i / C16;
-            j = i % C16;
-            const uint32_t t = fdiv(p, fd_wp);
-            const int xw = (int)(p - t * (uint32_t)wp);
-            const uint32_t b = fdiv(t, fd_hp);
-            const int yh = (int)(t - b * (uint32_t)hp);
-            const int iy = yh - pt, ix = xw - pl;
             uint4 out;
-            if (iy < 0 || iy >= h || ix < 0 || ix >= w) {  // zero-point border (axconv.py:185-189)
+            if (!inside) {
                 out = make_uint4(zpw, zpw, zpw, zpw);
                 s = zsum;
             } else {
-                const float4 *src = reinterpret_cast<const float4 *>(
-                    x + (((int64_t)b * h + iy) * w + ix) * c + j * 16);
-                float e[16];
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const float4 f = __ldg(src + v);
-                    e[4 * v] = f.x; e[4 * v + 1] = f.y; e[4 * v + 2] = f.z; e[4 * v + 3] = f.w;
-                }
                 int u[16];
                 bool ok = nearest;
 #pragma unroll
@@ -363,14 +369,16 @@ __global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__rest
             }
             reinterpret_cast<uint4 *>(codes)[i] = out;  // chunk i of the padded code tensor
         }
+        const uint32_t inext = i + stride;
+        inside = inext < total && fetch(inext, e);
         if constexpr (C16 > 1) {
 #pragma unroll
             for (int o = PER / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         }
         if constexpr (C16 <= 32) {
-            if (i < total && j == 0) pixsum[p] = s;
+            if (i < total && j == 0 && pixsum) pixsum[p] = s;
         } else {
-            if (i < total && (j & 31) == 0) atomicAdd(pixsum + p, s);  // pixsum zeroed on the host side
+            if (i < total && (j & 31) == 0 && pixsum) atomicAdd(pixsum + p, s);  // pixsum zeroed on the host side
         }
     }
     range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
@@ -723,7 +731,7 @@ static int quantize_pad_launch(const float *d_x, int64_t n, int64_t h, int64_t w
     const int64_t c16 = c / 16;
     if (c % 16 == 0 && c16 <= 32 && (c16 & (c16 - 1)) == 0 && ((reinterpret_cast<uintptr_t>(d_x) & 15) == 0)) {
         int64_t blocks = (total * c16 + 255) / 256;
-        const int64_t cap16 = (int64_t)sm_count() * 8;
+        const int64_t cap16 = (int64_t)sm_count() * 4;  // one resident wave: the prologue is paid once per CTA
         if (blocks > cap16) blocks = cap16;
 #define AXB_Q16(CC)                                                                                                 \
     quantize_pad16_kernel<CC><<<(int)blocks, 256, 0, s>>>(d_x, (int)n, (int)h, (int)w, pt, pl, (int)hp, (int)wp,    \
