@@ -100,7 +100,8 @@ int axb_params_upload(const axb_qparams *host_params, axb_qparams *d_params, voi
 
 /* ---- K2: quantize into a zero-point-padded uint8 NHWC tensor -------------- */
 /* d_x: (n,h,w,c) fp32; d_codes: (n, h+pt+pb, w+pl+pr, cs) raw code bytes with
- * the border = zero-point code and channels c..cs-1 = 0; d_pixsum: per padded
+ * the border = zero-point code and channels c..cs-1 = 0; d_pixsum (nullable: only the
+ * b-major-LUT kernel with K > 512 and the generic kernel read it): per padded
  * pixel sum of the c code values (int32).  cs = axb_channel_stride(c). */
 int64_t axb_channel_stride(int64_t c);
 int axb_quantize_pad(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, int32_t pt, int32_t pb,

@@ -605,6 +605,8 @@ int axb_conv2d_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
     if (fast) {
         // filter-specialised product table supplied (axb_ftable_prepare): the ftable kernel
         const bool use_ft = d->ftable != nullptr && d->variant == 0;
+        if (!use_ft && !d->pixsum && d->kpad > 512)
+            return set_error(AXB_E_VALUE, "the LUT kernel needs per-pixel code sums (pixsum) for this K");
         k.ftable = d->ftable;
         int v = d->variant;
         if (v < 0 || v >= kNumVariants) return set_error(AXB_E_VALUE, "unknown conv kernel variant");
@@ -639,6 +641,7 @@ int axb_conv2d_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
         }
         return AXB_OK;
     }
+    if (!d->pixsum) return set_error(AXB_E_VALUE, "the generic kernel needs per-pixel code sums (pixsum)");
     int64_t blocks = (M * d->cout + 255) / 256;
     const int64_t cap = (int64_t)sm_count() * 32;
     if (blocks > cap) blocks = cap;

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restri
             }
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (i < total && (i % G) == 0) pixsum[i / G] = s;
+            if (i < total && (i % G) == 0 && pixsum) pixsum[i / G] = s;
         }
     } else {
         const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restri
                 reinterpret_cast<uint32_t *>(codes + p * cs)[g] = group((uint32_t)p, (int)g, s);
 #pragma unroll
             for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) pixsum[p] = s;
+            if (lane == 0 && pixsum) pixsum[p] = s;
         }
     }
     range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);

@@ -131,21 +131,24 @@ class ConvLayer:
             d.kh = d.kw = d.sh = d.sw = d.dh = d.dw = 1
         else:
             codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
-            pixsum = torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
+            # the ftable kernel sums patch codes in its loop; only the LUT / generic kernels read pixsum
+            ft = self.ftable is not None and use_ftable and not variant and not force_generic
+            pixsum = None if ft else torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
+            pix_ptr = pixsum.data_ptr() if pixsum is not None else None
             if in_range_dev is not None:  # coefficients of the device range computed inside the quantize kernel
                 _lib.check(lib.axb_quantize_pad_range(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, in_range_dev,
                                                       self.sgn, self.round, self.params[0].data_ptr(),
-                                                      codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
+                                                      codes.data_ptr(), pix_ptr, qflag, stream))
             else:
                 _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs,
                                                 self.params[0].data_ptr(), self.sgn, self.round, codes.data_ptr(),
-                                                pixsum.data_ptr(), qflag, stream))
+                                                pix_ptr, qflag, stream))
             self.launches += 1
             d.n, d.hp, d.wp, d.cs, d.c = n, hp_, wp_, in_cs, c
             d.kh, d.kw = self.kh, self.kw
             d.sh, d.sw = g.strides
             d.dh, d.dw = g.dilations
-        d.codes, d.pixsum = codes.data_ptr(), pixsum.data_ptr()
+        d.codes, d.pixsum = codes.data_ptr(), (pixsum.data_ptr() if pixsum is not None else None)
         d.oh, d.ow = oh, ow
         d.fcodes, d.fsum = self.fcodes.data_ptr(), self.fsum.data_ptr()
         d.cout, d.coutp, d.kpad = self.cout, self.coutp, self.kpad
