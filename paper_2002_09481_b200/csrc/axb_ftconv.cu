@@ -383,6 +383,9 @@ static const FtVariant kFtVariants[] = {
     {"ft8_tm2_w16_k16", 2, 16, 4, 1, 1.127f},
     {"ft8_tm1_w8_k16", 1, 8, 4, 1, 1.556f},
     {"ft16_tm2_w16_k8_c2", 2, 16, 8, 2, 1.219f},
+    {"ft16_tm2_w12_k8", 2, 12, 8, 1, 1.050f},
+    {"ft16_tm3_w12_k8", 3, 12, 8, 1, 1.000f},
+    {"ft16_tm4_w12_k8", 4, 12, 8, 1, 1.000f},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
@@ -448,6 +451,9 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 5: return launch_ft<2, 16, 4, SGN, 1, 16, 3>(op, k, sm_limit, s, nm);
         case 6: return launch_ft<1, 8, 4, SGN, 1, 16, 3>(op, k, sm_limit, s, nm);
         case 7: return launch_ft<2, 16, 8, SGN, 2, 8, 3>(op, k, sm_limit, s, nm);
+        case 8: return launch_ft<2, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
+        case 9: return launch_ft<3, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
+        case 10: return launch_ft<4, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
