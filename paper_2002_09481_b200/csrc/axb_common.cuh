@@ -10,6 +10,12 @@ namespace axb {
 constexpr int kLutEntries = 65536;
 constexpr int kLutBytes = kLutEntries * 2;  // 128 KiB
 
+// ---- programmatic dependent launch: a kernel launched with the PDL attribute may start while
+// its predecessor is still running; it must wait before touching the predecessor's outputs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// let the next (PDL-launched) kernel be scheduled as soon as this grid's CTAs start retiring
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+
 // ---- ordered-float <-> int (monotone map so atomicMin/Max on int == float min/max)
 __host__ __device__ __forceinline__ int32_t f2ord(float f) {
 #ifdef __CUDA_ARCH__

@@ -139,6 +139,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
         }
     };
     // loader: runs PF chunks ahead of the consumer, across tile boundaries
+    // everything above (barrier init, tap table, the first table stages in flight) overlaps the
+    // predecessor's tail; its outputs (codes, qparams, residual, ranges) are read only after this
+    pdl_wait();
     uint4 av[PF][TM];
     int ld_t = 0, ld_ci = 0, ld_kc = 0;  // tap, channel offset and index of the next chunk to load
     int64_t ld_left = my_tiles * p.nchunks, ld_tile = cid;
@@ -400,16 +403,18 @@ static int launch_ft(int op, const ConvK &k, int sm_limit, cudaStream_t s, const
     int dev = 0;
     cudaGetDevice(&dev);
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (pdl_wait in the kernel)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CL;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.blockDim = dim3(WARPS * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = CL > 1 ? 1 : 0;
+    cfg.numAttrs = CL > 1 ? 2 : 1;
     if (configured_dev != dev) {
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_ft");

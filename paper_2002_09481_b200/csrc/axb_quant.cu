@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__rest
                                                              int32_t *__restrict__ pixsum, int32_t *d_flags) {
     __shared__ QuantCtx q;
     const int c = 16 * C16;
+    pdl_launch_dependents();  // the next conv may start its prologue (table TMA) as CTAs retire
     const uint32_t npix = (uint32_t)n * (uint32_t)hp * (uint32_t)wp;
     constexpr int PER = C16 <= 32 ? C16 : 32;  // lanes per pixel in the segmented sum
     const uint32_t total = npix * (uint32_t)C16;
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(QT_H *QT_W) quantize_im2col_kernel(
     int is_signed, int round_mode, uint8_t *__restrict__ rows, int32_t *__restrict__ rowsum, int32_t *d_flags) {
     __shared__ QuantCtx q;
     __shared__ uint8_t patch[kQiPatchMax];
+    pdl_launch_dependents();
     __shared__ int16_t koff[kMaxIm2colK];  // patch offset of window element k = (ky, kx, ci)
     if (d_range)
         quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
