@@ -98,7 +98,8 @@ class GpuGraph:
                  in_shape=None, sm_limit: int = 0, variant: int = 0):
         if not torch.cuda.is_available():
             raise _lib.AxbError("GpuGraph needs a CUDA device (no CPU fallback)")
-        self.nodes = list(nodes)
+        # node dicts; kinds may be the reference's NodeKind enum or its string value
+        self.nodes = [dict(n, kind=getattr(n["kind"], "value", n["kind"])) for n in nodes]
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.acc_name = _mode_value(accumulator)
         self.round_name = _mode_value(round_mode)
@@ -195,6 +196,9 @@ class GpuGraph:
                 self.steps.append(_Step("conv", n, conv_plans[n["id"]]))
             elif kind in ("Input", "ReLU", "Add", "MaxPool", "AvgPool", "Flatten", "Dense", "Softmax"):
                 self.steps.append(_Step(kind, n))
+            elif kind == "Conv2D":
+                raise ValueError(f"Conv2D node {n['id']!r}: GpuGraph runs transformed graphs "
+                                 "(model.transform replaces Conv2D by Min/Max/AxConv2D, graph.py:107-141)")
             else:
                 raise ValueError(f"unsupported node kind {kind!r}")
         self.conv_plans = conv_plans
