@@ -160,7 +160,9 @@ int axb_conv2d_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);
 /* ---- filter-specialised product table (once per layer and truth table) -----
  * The filter codes of a layer are constants (graph.py:129-130), so the 256
  * possible products of every filter code are gathered once:
- *   W[nb][k][pair][a] = u(lut[(a<<8)|F[k][nb*16+2*pair]]) | u(lut[(a<<8)|F[k][nb*16+2*pair+1]]) << 16
+ *   W[sb][k][pair][a] = u(lut[(a<<8)|F[k][sb*8+2*pair]]) | u(lut[(a<<8)|F[k][sb*8+2*pair+1]]) << 16
+ * (sb = 8-channel sub-block, pair = 0..3: 4 KiB per (sb, k) row; a conv tile of 8 or 16
+ * channels streams one or two sub-blocks' rows)
  * (u = raw ^ 0x8000 for signed tables, raw for unsigned; junk rows = zero
  * contribution), uint32, axb_ftable_bytes(kpad, coutp) = kpad * coutp * 512 bytes.
  * kh, kw, c, cs are the filter geometry the conv sees (as axb_filters_prepare).
