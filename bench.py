@@ -430,6 +430,18 @@ def main():
         except Exception:
             traffic = None
     kernels = sorted({k for *_, k in profile})
+    # measured bank-conflict share of the kernel's shared-memory wavefronts (committed ncu capture):
+    # with the LDS pipe 100% busy the kernel could reach at most (1 - conflict) of `peak`
+    conflict = None
+    cf = ROOT / "profiles" / "conflicts_p12.json"
+    if cf.exists():
+        try:
+            launches = _json.loads(cf.read_text()).get("r8" if args.workload == "r8" else "r50", [])
+            if launches:
+                conflict = sum(x["bank_conflict_wavefronts"] for x in launches) / sum(
+                    x["shared_ld_wavefronts"] for x in launches)
+        except Exception:
+            conflict = None
     roofline = {
         "bound": "smem", "kernel": "LUT-product gather conv, all conv launches of a step: " + ", ".join(kernels),
         "achieved": round(achieved / 1e9, 2), "peak": round(peak_lookups / 1e9, 2), "unit": "Glookup/s",
@@ -437,6 +449,9 @@ def main():
         "frac_at_sampled_clock": round(achieved / (sm_count * 64 * sampled * 1e6), 4) if sampled else None,
         "peak_basis": f"derived: {sm_count} SMs x 128 B/clk shared-memory bandwidth / 2 B per 16-bit product "
                       f"= 64 lookups/clk/SM x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+        "lds_conflict_wavefront_frac": round(conflict, 4) if conflict is not None else None,
+        "frac_of_conflict_bound": round(achieved / peak_lookups / (1 - conflict), 4) if conflict else None,
+        "conflict_basis": "profiles/conflicts_p12.json (ncu l1tex shared-load bank conflicts / wavefronts)",
         "lds16_lookup_roofline": round(lds16_lookups / 1e9, 2),
         "frac_vs_lds16_lookup_roofline": round(achieved / lds16_lookups, 4),
         "traffic": traffic, "traffic_unit": "DRAM bytes per LUT-conv launch (ncu --set full, committed profile)",
