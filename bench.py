@@ -433,7 +433,7 @@ def main():
     # measured bank-conflict share of the kernel's shared-memory wavefronts (committed ncu capture):
     # with the LDS pipe 100% busy the kernel could reach at most (1 - conflict) of `peak`
     conflict = None
-    cf = ROOT / "profiles" / "conflicts_p12.json"
+    cf = ROOT / "profiles" / "conflicts.json"
     if cf.exists():
         try:
             launches = _json.loads(cf.read_text()).get("r8" if args.workload == "r8" else "r50", [])
@@ -451,7 +451,7 @@ def main():
                       f"= 64 lookups/clk/SM x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
         "lds_conflict_wavefront_frac": round(conflict, 4) if conflict is not None else None,
         "frac_of_conflict_bound": round(achieved / peak_lookups / (1 - conflict), 4) if conflict else None,
-        "conflict_basis": "profiles/conflicts_p12.json (ncu l1tex shared-load bank conflicts / wavefronts)",
+        "conflict_basis": "profiles/conflicts.json (ncu l1tex shared-load bank conflicts / wavefronts)",
         "lds16_lookup_roofline": round(lds16_lookups / 1e9, 2),
         "frac_vs_lds16_lookup_roofline": round(achieved / lds16_lookups, 4),
         "traffic": traffic, "traffic_unit": "DRAM bytes per LUT-conv launch (ncu --set full, committed profile)",
