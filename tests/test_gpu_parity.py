@@ -649,3 +649,20 @@ def test_r50_autotune_all_variants_agree():
     for _ in range(2):
         g.autotune(x, reps=1)
         assert torch.equal(g.run(x).view(torch.int32), want.view(torch.int32))
+
+
+@pytest.mark.parametrize("cand", [5, 14, 22, 31])
+def test_sweep_candidate_networks_vs_oracle(cand):
+    """Config 4: a ResNet-62 built on a sweep candidate table (truncated / error-injected, both
+    signedness) gives the oracle graph's logits bit for bit (2 CIFAR-shaped images)."""
+    torch = _torch()
+    from bench import oracle_nodes, sweep_luts
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200.datasets import synthetic_cifar10
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    nodes = resnet.cifar_resnet(10, sweep_luts()[cand], seed=0)
+    x, _ = synthetic_cifar10(2, seed=77)
+    want = O.run_graph(oracle_nodes(nodes), x)
+    got = GpuGraph(nodes).run(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert bits_equal(got, want)
