@@ -24,15 +24,19 @@
 // A = sum u - kpad * 32768 (signed) -- bit-identical int sums.  Junk rows
 // (channel / K padding) hold the zero contribution (u = bias) for every a.
 //
-// Layout in HBM (uint32): [nb = coutp/16][k = 0..kpad-1][pair = 0..7][a = 0..255],
-// i.e. 8 KiB per (channel block, row).  A pipeline stage is KS consecutive rows
-// of one channel block (KS * 8 KiB, contiguous) moved by ONE TMA bulk copy
-// (cp.async.bulk + mbarrier complete_tx) into a ring of ST stages; consumers
-// release a stage with one mbarrier arrive per warp.  Activation codes are read
-// straight from the zp-padded NHWC code tensor into registers (one LDG.128 =
-// 16 rows of one pixel), one 16-row chunk ahead.
+// Layout in HBM (uint32): [sb = coutp/8][k = 0..kpad-1][pair = 0..3][a = 0..255], i.e. 4 KiB
+// per (8-channel sub-block, row).  A tile of 8 or 16 channels (NPB = 4 or 8 pairs) streams KS
+// consecutive rows of its one or two sub-blocks per pipeline stage, moved by TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx) into a ring of ST stages.  Thread 0 refills the slot
+// of stage g-1 at the start of stage g, after every warp released it: each lane executes
+// fence.proxy.async (its generic-proxy LDS reads before the async-proxy refill), then lane 0
+// arrives on the slot's "empty" mbarrier.  Activation codes are read straight from the
+// zp-padded NHWC code tensor into registers (one LDG.128 = 16 rows of one pixel), one 16-row
+// chunk ahead, across tile boundaries.  The kernel is launched with programmatic dependent
+// launch: barrier init, the tap table and the first table stages overlap the previous
+// kernel's tail (pdl_wait before the first activation load).
 //
-// Tiles: BM = WARPS*32*TM output pixels x 16 channels; tile = nb * ntm + mt, so
+// Tiles: BM = WARPS*32*TM output pixels x BN = 2*NPB channels; tile = nb * ntm + mt, so
 // the CTAs running concurrently share one channel block's table rows in L2.
 #include "axb_convk.cuh"
 
