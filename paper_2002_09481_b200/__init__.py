@@ -10,6 +10,8 @@ Public API (mirrors the reference names):
   Tensor4, Range, ConvGeometry, ConvConfig, MultLut, Signedness, RoundMode,
   Accumulator, QuantParams, compute_coeffs, exact_lut, truncated_lut, ...
   graph.GpuGraph / graph.run                    -- GPU executor for AxConv2D graphs
+  model.transform / save_model / load_model     -- Conv2D -> AxConv2D, model files
+  formats.*                                     -- .axm / .axt / CIFAR-10 / report files
   resnet.*                                      -- ResNet graph builders (benchmarks)
 """
 
@@ -28,6 +30,7 @@ from .types import (  # noqa: F401
     conv_mac_count,
     exact_lut,
     output_shape,
+    perturbed_lut,
     random_lut,
     resolve_padding,
     stitch_index,
