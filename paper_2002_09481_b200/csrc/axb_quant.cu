@@ -731,7 +731,10 @@ static int quantize_pad_launch(const float *d_x, int64_t n, int64_t h, int64_t w
     if (total * (cs / 4) >= (int64_t(1) << 31)) return set_error(AXB_E_VALUE, "quantize: more than 2^31 code words");
     const FastDiv fhp = make_fastdiv((uint32_t)hp), fwp = make_fastdiv((uint32_t)wp);
     const int64_t c16 = c / 16;
-    if (c % 16 == 0 && c16 <= 32 && (c16 & (c16 - 1)) == 0 && ((reinterpret_cast<uintptr_t>(d_x) & 15) == 0)) {
+    if (c % 16 == 0 && c16 <= 128 && (c16 & (c16 - 1)) == 0 && ((reinterpret_cast<uintptr_t>(d_x) & 15) == 0)) {
+        // wide pixels (c = 1024, 2048): one warp per 32 chunks, per-pixel sums by atomics into a zeroed buffer
+        if (c16 > 32 && d_pixsum && cudaMemsetAsync(d_pixsum, 0, total * 4, s) != cudaSuccess)
+            return set_error(AXB_E_CUDA, "pixsum clear failed");
         int64_t blocks = (total * c16 + 255) / 256;
         const int64_t cap16 = (int64_t)sm_count() * 4;  // one resident wave: the prologue is paid once per CTA
         if (blocks > cap16) blocks = cap16;
@@ -745,7 +748,9 @@ static int quantize_pad_launch(const float *d_x, int64_t n, int64_t h, int64_t w
             case 4: AXB_Q16(4); break;
             case 8: AXB_Q16(8); break;
             case 16: AXB_Q16(16); break;
-            default: AXB_Q16(32); break;
+            case 32: AXB_Q16(32); break;
+            case 64: AXB_Q16(64); break;
+            default: AXB_Q16(128); break;
         }
 #undef AXB_Q16
         return check_launch("quantize_pad16");

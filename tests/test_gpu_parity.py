@@ -666,3 +666,22 @@ def test_sweep_candidate_networks_vs_oracle(cand):
     want = O.run_graph(oracle_nodes(nodes), x)
     got = GpuGraph(nodes).run(torch.from_numpy(x).cuda()).cpu().numpy()
     assert bits_equal(got, want)
+
+
+@pytest.mark.parametrize("c", [1024, 2048])
+def test_wide_channel_quantize_and_lut_kernel_pixsum(c):
+    """c = 1024 / 2048 inputs (ResNet-50 stage 3/4): the 16-channel-chunk quantizer with atomic
+    per-pixel sums, read by the b-major LUT kernel (K > 512 -> sums gathered in the epilogue), and
+    the ftable path -- both equal to the oracle bit for bit."""
+    rng = np.random.default_rng(c)
+    case = dict(x=np.maximum(rng.standard_normal((2, 5, 4, c)), 0).astype(np.float32),
+                f=(rng.standard_normal((1, 1, c, 24)) * 0.05).astype(np.float32), lut=O.random_lut(rng, O.SIGNED),
+                mode=O.SIGNED, padding="same", strides=(1, 1), dilations=(1, 1), accumulator=O.EXACT64,
+                round_mode=O.HALF_AWAY)
+    case.update(in_range=(float(case["x"].min()), float(case["x"].max())),
+                f_range=(float(case["f"].min()), float(case["f"].max())))
+    want, want_acc = oracle_conv(case, return_acc=True)
+    for use_ft in (False, True):
+        y, acc, kern = gpu_conv(case, use_ftable=use_ft)
+        assert bits_equal(y, want), kern
+        assert np.array_equal(acc, want_acc), kern
