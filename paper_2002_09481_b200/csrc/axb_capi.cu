@@ -86,6 +86,66 @@ __global__ void maxpool_kernel(const float *__restrict__ x, int64_t n, int64_t h
     range_commit(tmin, tmax, nonfinite, d_range, d_flags, AXB_FLAG_OUT_NONFINITE);
 }
 
+// Vectorised pools for c % 4 == 0: one thread per (output pixel, 4 channels), float4 loads and
+// stores, 32-bit magic-number index division (the scalar kernels above spend most of their time
+// in 64-bit div/mod).  Identical per-element arithmetic and order.
+template <bool MAX>
+__global__ void __launch_bounds__(256) pool4_kernel(const float4 *__restrict__ x, int h, int w, int c4, int ph,
+                                                    int pw, int sh, int sw, int pt, int pl, int oh, int ow,
+                                                    uint32_t total, FastDiv fd_c4, FastDiv fd_ow, FastDiv fd_oh,
+                                                    float4 *__restrict__ out, int32_t *d_range, int32_t *d_flags) {
+    int32_t tmin = INT32_MAX, tmax = INT32_MIN;
+    int nonfinite = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t t = fdiv(i, fd_c4);
+        const int cg = (int)(i - t * (uint32_t)c4);
+        const uint32_t t2 = fdiv(t, fd_ow);
+        const int ox = (int)(t - t2 * (uint32_t)ow);
+        const uint32_t b = fdiv(t2, fd_oh);
+        const int oy = (int)(t2 - b * (uint32_t)oh);
+        float r[4];
+        int valid = 0;
+        bool first = true;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = MAX ? -INFINITY : 0.0f;
+        for (int ky = 0; ky < ph; ++ky) {
+            const int iy = oy * sh + ky - pt;
+            for (int kx = 0; kx < pw; ++kx) {
+                const int ix = ox * sw + kx - pl;
+                const bool in = iy >= 0 && iy < h && ix >= 0 && ix < w;
+                float4 v4 = make_float4(MAX ? -INFINITY : 0.0f, MAX ? -INFINITY : 0.0f, MAX ? -INFINITY : 0.0f,
+                                        MAX ? -INFINITY : 0.0f);
+                if (in) v4 = __ldg(x + (((int64_t)b * h + iy) * w + ix) * c4 + cg);
+                const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (MAX) {
+                        if (r[j] == r[j] && (v[j] > r[j] || v[j] != v[j])) r[j] = v[j];  // np.max, NaN wins
+                    } else {
+                        const float u = v[j] != v[j] ? 0.0f : v[j];  // nansum
+                        r[j] = first ? u : __fadd_rn(r[j], u);
+                    }
+                }
+                valid += in;
+                first = false;
+            }
+        }
+        if (!MAX) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) r[j] = __double2float_rn((double)r[j] / (double)valid);
+        }
+        out[i] = make_float4(r[0], r[1], r[2], r[3]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            nonfinite |= !isfinite(r[j]);
+            const int32_t o = f2ord(r[j]);
+            tmin = min(tmin, o);
+            tmax = max(tmax, o);
+        }
+    }
+    range_commit(tmin, tmax, nonfinite, d_range, d_flags, AXB_FLAG_OUT_NONFINITE);
+}
+
 // AvgPool (graph.py:193-199): nansum in sequential (ky, kx) fp32 order (padding
 // taps add +0.0), then float32 / int64 -> float64 division, narrowed to fp32.
 __global__ void avgpool_kernel(const float *__restrict__ x, int64_t n, int64_t h, int64_t w, int64_t c, int ph,
@@ -209,6 +269,15 @@ int axb_maxpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, in
                 int32_t *d_flags, void *stream) {
     const int64_t total = n * oh * ow * c;
     if (total == 0) return AXB_OK;
+    if (c % 4 == 0 && total / 4 < (int64_t(1) << 32) && ((reinterpret_cast<uintptr_t>(d_x) |
+                                                            reinterpret_cast<uintptr_t>(d_out)) & 15) == 0) {
+        const uint32_t t4 = (uint32_t)(total / 4);
+        pool4_kernel<true><<<grid_for(t4), 256, 0, (cudaStream_t)stream>>>(
+            reinterpret_cast<const float4 *>(d_x), (int)h, (int)w, (int)(c / 4), ph, pw, sh, sw, pt, pl, (int)oh,
+            (int)ow, t4, make_fastdiv((uint32_t)(c / 4)), make_fastdiv((uint32_t)ow), make_fastdiv((uint32_t)oh),
+            reinterpret_cast<float4 *>(d_out), d_out_range, d_flags);
+        return check_launch("maxpool4");
+    }
     maxpool_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(d_x, n, h, w, c, ph, pw, sh, sw, pt, pl, oh,
                                                                        ow, d_out, d_out_range, d_flags);
     return check_launch("maxpool");
@@ -219,6 +288,15 @@ int axb_avgpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, in
                 int32_t *d_flags, void *stream) {
     const int64_t total = n * oh * ow * c;
     if (total == 0) return AXB_OK;
+    if (c % 4 == 0 && total / 4 < (int64_t(1) << 32) && ((reinterpret_cast<uintptr_t>(d_x) |
+                                                            reinterpret_cast<uintptr_t>(d_out)) & 15) == 0) {
+        const uint32_t t4 = (uint32_t)(total / 4);
+        pool4_kernel<false><<<grid_for(t4), 256, 0, (cudaStream_t)stream>>>(
+            reinterpret_cast<const float4 *>(d_x), (int)h, (int)w, (int)(c / 4), ph, pw, sh, sw, pt, pl, (int)oh,
+            (int)ow, t4, make_fastdiv((uint32_t)(c / 4)), make_fastdiv((uint32_t)ow), make_fastdiv((uint32_t)oh),
+            reinterpret_cast<float4 *>(d_out), d_out_range, d_flags);
+        return check_launch("avgpool4");
+    }
     avgpool_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(d_x, n, h, w, c, ph, pw, sh, sw, pt, pl, oh,
                                                                        ow, d_out, d_out_range, d_flags);
     return check_launch("avgpool");

@@ -685,3 +685,28 @@ def test_wide_channel_quantize_and_lut_kernel_pixsum(c):
         y, acc, kern = gpu_conv(case, use_ftable=use_ft)
         assert bits_equal(y, want), kern
         assert np.array_equal(acc, want_acc), kern
+
+
+@pytest.mark.parametrize("kind", ["MaxPool", "AvgPool"])
+@pytest.mark.parametrize("c", [3, 16, 64])
+def test_pools_match_oracle(kind, c):
+    """MaxPool / AvgPool (graph.py:182-199) through the executor vs the oracle, bit for bit: valid and
+    explicit/same padding, strided and global windows, NaN and inf inputs (c % 4 == 0 takes the
+    vectorised kernel, c = 3 the scalar one)."""
+    torch = _torch()
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    rng = np.random.default_rng(c)
+    x = rng.standard_normal((3, 9, 11, c)).astype(np.float32)
+    x[0, 1, 2, 0] = np.nan
+    x[1, 4, 4, c - 1] = np.inf
+    x[2, 8, 10, 0] = -np.inf
+    for attrs in ({"pool": [3, 3], "strides": [2, 2], "padding": "same"},
+                  {"pool": [2, 2], "strides": [2, 2], "padding": "valid"},
+                  {"pool": [3, 2], "strides": [1, 2], "padding": [1, 0, 1, 1]},
+                  {"pool": [9, 11], "strides": [9, 11], "padding": "valid"}):
+        nodes = [{"id": "in", "kind": "Input", "inputs": [], "attrs": {}},
+                 {"id": "p", "kind": kind, "inputs": ["in"], "attrs": dict(attrs)}]
+        got = GpuGraph(nodes).run(torch.from_numpy(x).cuda(), check=False).cpu().numpy()
+        want = O.pool2d(x, attrs, kind == "MaxPool")
+        assert bits_equal(got, want), (kind, c, attrs)
