@@ -710,3 +710,24 @@ def test_pools_match_oracle(kind, c):
         got = GpuGraph(nodes).run(torch.from_numpy(x).cuda(), check=False).cpu().numpy()
         want = O.pool2d(x, attrs, kind == "MaxPool")
         assert bits_equal(got, want), (kind, c, attrs)
+
+
+@pytest.mark.parametrize("mode", [O.SIGNED, O.UNSIGNED])
+def test_ftable_kernel_long_k_packed_sums_exact(mode):
+    """K = 3*3*2048 = 18,432 taps with full-range random 16-bit products: the packed-pair sums
+    (sum of high halves up to 1.2e9) and the epilogue stay exact on every ftable variant."""
+    from paper_2002_09481_b200 import _lib
+
+    rng = np.random.default_rng(18432 + (mode == O.SIGNED))
+    case = dict(x=rng.uniform(-1, 3, (1, 3, 4, 2048)).astype(np.float32),
+                f=rng.standard_normal((3, 3, 2048, 20)).astype(np.float32), lut=O.random_lut(rng, mode),
+                mode=mode, padding="same", strides=(1, 1), dilations=(1, 1), accumulator=O.WRAP32,
+                round_mode=O.HALF_EVEN)
+    case.update(in_range=(float(case["x"].min()), float(case["x"].max())),
+                f_range=(float(case["f"].min()), float(case["f"].max())))
+    want, want_acc = oracle_conv(case, return_acc=True)
+    for v in range(1, _lib.load().axb_ft_variant_count()):
+        y, acc, kern = gpu_conv(case, ft_variant=v)
+        assert kern.startswith("ft"), kern
+        assert bits_equal(y, want), kern
+        assert np.array_equal(acc, want_acc), kern
