@@ -265,7 +265,8 @@ def main():
         val = statistics.median(steps)
         line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GMAC/s",
                 "images_per_s": round(val * 1e9 / macs_img, 3), "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "warmup": args.warmup, "higher_is_better": True,
+                "scaling": "strong" if spec.get("sweep") else "weak", "vs_baseline": None,
                 "dtype": "u8", "data": "synthetic",
                 "config": {"workload": spec["desc"], "batch_per_gpu": batch, "lut": spec["lut"]},
                 "cpu_baseline": {"value": val, "unit": "GMAC/s", "cores": info["cores"], "kind": "port",
@@ -463,7 +464,8 @@ def main():
         "metric": METRIC, "value": round(gmacs, 2), "unit": "GMAC/s",
         "images_per_s": round(images / (total_ms / 1e3), 2), "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak",
+        # range-batches: fixed batch per GPU (weak); the 32-table sweep: fixed job split over ranks (strong)
+        "scaling": "strong" if spec.get("sweep") else "weak",
         "vs_baseline": round(gmacs / PAPER_GMACS[args.workload], 2) if args.workload in PAPER_GMACS else None,
         "vs_baseline_basis": "paper-derived GTX 1080 approx GMAC/s (BASELINE.md s1)" if args.workload in PAPER_GMACS else None,
         "dtype": "u8", "data": "synthetic",
