@@ -419,8 +419,17 @@ def main():
     # 32 four-byte banks) / 2 B per 16-bit product = 64 lookups/clk/SM.  The ftable kernel reaches it
     # with two products per bank word; the north_star's LDS.16 roofline (one lookup per lane per
     # wavefront, 32/clk/SM) is reported alongside.
-    peak_lookups = sm_count * 64 * max_mhz * 1e6
+    theo_lookups = sm_count * 64 * max_mhz * 1e6
     lds16_lookups = sm_count * 32 * max_mhz * 1e6
+    # measured shared-memory gather roofline (scripts/smem_roofline.cu): conflict-free warp gathers
+    # of 64/128-bit words = the bandwidth bound as this B200 delivers it; LDS.32 with the kernel's
+    # packed-pair accumulation mix alongside
+    measured = {}
+    try:
+        measured = _json.loads((ROOT / "profiles" / "smem_roofline.json").read_text())["products_per_s"]
+    except Exception:
+        measured = {}
+    peak_lookups = max(measured.get("lds64", 0.0), measured.get("lds128", 0.0)) or theo_lookups
     achieved = conv_macs / (conv_ms / 1e3) if conv_ms else 0.0
     sampled = clocks.get("sm_mhz")
     traffic = None
@@ -447,11 +456,15 @@ def main():
         "bound": "smem", "kernel": "LUT-product gather conv, all conv launches of a step: " + ", ".join(kernels),
         "achieved": round(achieved / 1e9, 2), "peak": round(peak_lookups / 1e9, 2), "unit": "Glookup/s",
         "frac": round(achieved / peak_lookups, 4),
-        "frac_at_sampled_clock": round(achieved / (sm_count * 64 * sampled * 1e6), 4) if sampled else None,
-        "peak_basis": f"derived: {sm_count} SMs x 128 B/clk shared-memory bandwidth / 2 B per 16-bit product "
-                      f"= 64 lookups/clk/SM x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+        "frac_at_sampled_clock": round(achieved / peak_lookups * max_mhz / sampled, 4) if sampled else None,
+        "peak_basis": ("measured: conflict-free LDS.64/LDS.128 warp gathers of 16-bit products "
+                       "(profiles/smem_roofline.json, scripts/smem_roofline.cu)") if measured else
+                      (f"derived: {sm_count} SMs x 128 B/clk / 2 B per product x {max_mhz:.0f} MHz"),
+        "peak_theoretical": round(theo_lookups / 1e9, 2),
+        "peak_lds32_gather_measured": round(measured["lds32"] / 1e9, 2) if measured else None,
+        "frac_of_lds32_gather_peak": round(achieved / measured["lds32"], 4) if measured else None,
         "lds_conflict_wavefront_frac": round(conflict, 4) if conflict is not None else None,
-        "frac_of_conflict_bound": round(achieved / peak_lookups / (1 - conflict), 4) if conflict else None,
+        "frac_of_conflict_bound": round(achieved / theo_lookups / (1 - conflict), 4) if conflict else None,
         "conflict_basis": "profiles/conflicts.json (ncu l1tex shared-load bank conflicts / wavefronts)",
         "lds16_lookup_roofline": round(lds16_lookups / 1e9, 2),
         "frac_vs_lds16_lookup_roofline": round(achieved / lds16_lookups, 4),
