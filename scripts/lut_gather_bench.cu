@@ -1,0 +1,92 @@
+// A/B of the product-gather inner loop on REAL activation codes (ResNet-8 s0b0.b input, 4x8 pixel
+// blocks x 16 taps per group; build/codes_s0b0b.bin from the oracle): lanes = pixels, 16 channels.
+//   W2: 32-bit words = 2 channels per code (8 LDS.32 per pixel-tap)   -- the shipped ftable layout
+//   W4: 64-bit words = 4 channels per code (4 LDS.64 per pixel-tap)
+// Packed-pair accumulation as in lutconv_ft.  Prints products/s for both.
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+constexpr int ROWS = 4;                 // table rows cycled over the 16 taps
+constexpr int ROW_WORDS = 256 * 8;      // 8 pairs x 256 codes (8 KiB) in both layouts
+constexpr int REPS = 8;
+
+template <int W4>
+__global__ void __launch_bounds__(512, 1) bench(const uint4 *__restrict__ codes, int groups, uint32_t *out) {
+    __shared__ __align__(16) uint32_t tab[ROWS * ROW_WORDS];
+    for (int i = threadIdx.x; i < ROWS * ROW_WORDS; i += blockDim.x) tab[i] = i * 2654435761u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    uint32_t all[8] = {0}, hi[8] = {0};
+    for (int rep = 0; rep < REPS; ++rep) {
+        for (int g = warp; g < groups; g += nwarps) {
+            const uint4 c = __ldg(codes + g * 32 + lane);
+            const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t a = __byte_perm(cw[k >> 2], 0, 0x4440u + (k & 3));
+                const uint32_t *row = tab + (k % ROWS) * ROW_WORDS;
+                if (!W4) {
+                    const uint32_t *base = row + a;  // [pair][a]: pair stride 256 words
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) {
+                        const uint32_t w = base[p * 256];
+                        all[p] += w; hi[p] += w >> 16;
+                    }
+                } else {
+                    const uint2 *base = reinterpret_cast<const uint2 *>(row) + a;  // [quad][a]: 8 B entries
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint2 w = base[q * 256];
+                        all[2 * q] += w.x; hi[2 * q] += w.x >> 16;
+                        all[2 * q + 1] += w.y; hi[2 * q + 1] += w.y >> 16;
+                    }
+                }
+            }
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) s += all[p] ^ hi[p];
+    if (s == 0x12345678u) out[0] = s;
+}
+
+int main() {
+    FILE *f = fopen("build/codes_s0b0b.bin", "rb");
+    if (!f) { printf("{\"error\": \"build/codes_s0b0b.bin missing\"}\n"); return 1; }
+    std::vector<uint8_t> h(1 << 25);
+    const size_t n = fread(h.data(), 1, h.size(), f);
+    fclose(f);
+    const int groups = (int)(n / (32 * 16));
+    uint4 *d;
+    cudaMalloc(&d, n);
+    cudaMemcpy(d, h.data(), n, cudaMemcpyHostToDevice);
+    uint32_t *out;
+    cudaMalloc(&out, 4);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    for (int i = 0; i < 5; ++i) bench<1><<<sms, 512>>>(d, groups, out);
+    cudaDeviceSynchronize();
+    double best[2] = {0, 0};
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int it = 0; it < 3; ++it) {
+        for (int w4 = 0; w4 < 2; ++w4) {
+            cudaEventRecord(a);
+            if (w4) bench<1><<<sms, 512>>>(d, groups, out); else bench<0><<<sms, 512>>>(d, groups, out);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, a, b);
+            const double prod = (double)groups * 32 * 16 * 16 * REPS / (ms * 1e-3);
+            if (prod > best[w4]) best[w4] = prod;
+        }
+    }
+    printf("{\"codes\": \"ResNet-8 s0b0.b input, 4x8 blocks\", \"groups\": %d, \"W2_lds32_products_per_s\": %.4e, "
+           "\"W4_lds64_products_per_s\": %.4e}\n", groups, best[0], best[1]);
+    return 0;
+}
