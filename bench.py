@@ -239,6 +239,9 @@ def main():
     ap.add_argument("--no-autotune", action="store_true", help="use the cost model's kernel variants")
     ap.add_argument("--tuned-out", default="", help="write the autotuned per-layer variants (json)")
     ap.add_argument("--tuned-from", default="", help="use per-layer variants from a --tuned-out file")
+    ap.add_argument("--report-out", default="",
+                    help="also write a RunReport (t_init + t_comp, phase split; reference bench.py:37-87) of "
+                         "benchmark.run_benchmark over --steps batches: <path>.json and <path>.csv")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -388,6 +391,15 @@ def main():
     for o, t in zip(outs, ys):  # the host logits of the last e2e step == the device-timed run's
         assert torch.equal(o[-1].view(torch.int32), t.cpu().view(torch.int32))
 
+    if args.report_out and rank == 0:  # the reference harness's report, from the GPU engine (outside the region)
+        from paper_2002_09481_b200.benchmark import run_benchmark
+        from paper_2002_09481_b200.formats import report_csv, save_report
+
+        report, _ = run_benchmark(graphs[0], np.concatenate([host_np] * args.steps), batch_size=batch,
+                                  batches=args.steps)
+        save_report(report, args.report_out + ".json")
+        Path(args.report_out + ".csv").write_text(report_csv(report))
+
     # ------------------------------------------------ max over ranks, NCCL gather of logits/counts
     from paper_2002_09481_b200.dist import exchange_results
 
@@ -446,10 +458,10 @@ def main():
     cf = ROOT / "profiles" / "conflicts.json"
     if cf.exists():
         try:
-            launches = _json.loads(cf.read_text()).get("r8" if args.workload == "r8" else "r50", [])
-            if launches:
-                conflict = sum(x["bank_conflict_wavefronts"] for x in launches) / sum(
-                    x["shared_ld_wavefronts"] for x in launches)
+            captured = _json.loads(cf.read_text()).get("r8" if args.workload == "r8" else "r50", [])
+            if captured:
+                conflict = sum(x["bank_conflict_wavefronts"] for x in captured) / sum(
+                    x["shared_ld_wavefronts"] for x in captured)
         except Exception:
             conflict = None
     roofline = {

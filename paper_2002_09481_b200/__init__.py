@@ -12,6 +12,7 @@ Public API (mirrors the reference names):
   graph.GpuGraph / graph.run                    -- GPU executor for AxConv2D graphs
   model.transform / save_model / load_model     -- Conv2D -> AxConv2D, model files
   formats.*                                     -- .axm / .axt / CIFAR-10 / report files
+  benchmark.run_benchmark / speedup             -- t_init + t_comp RunReport on the GPU engine
   resnet.*                                      -- ResNet graph builders (benchmarks)
 """
 

@@ -249,11 +249,14 @@ class GpuGraph:
 
     # ------------------------------------------------------------------ execution
     def run(self, batch: torch.Tensor, check: bool = True, trace: dict | None = None,
-            profile: list | None = None) -> torch.Tensor:
+            profile: list | None = None, timeline: list | None = None) -> torch.Tensor:
         """Evaluate on a (n,h,w,c) fp32 CUDA batch; returns the last node's value.
 
-        ``profile`` (a list) receives (node_id, start_event, end_event, macs)
-        around every LUT-conv kernel launch, for live per-kernel timing.
+        ``profile`` (a list) receives (node_id, start_event, end_event, macs, ...)
+        around every LUT-conv kernel launch, for live per-kernel timing;
+        ``timeline`` (a list) receives (node_id, step_kind, start_event, end_event)
+        around every executed node (the GPU counterpart of ``Meter.node``,
+        metering.py:39-46; ``benchmark.run_benchmark`` turns both into a RunReport).
         """
         records = batch.dtype == torch.uint8
         if records:  # CIFAR-10 binary records (n, 3073): decoded on the device (formats.py:138-157)
@@ -298,6 +301,9 @@ class GpuGraph:
         for st in self.steps:
             n = st.node
             nid = n["id"]
+            if timeline is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
             if st.kind == "Input" and records:
                 images = torch.empty(in_shape, dtype=torch.float32, device=self.device)
                 if self.labels is None or self.labels.numel() != in_shape[0]:
@@ -357,6 +363,10 @@ class GpuGraph:
             elif st.kind == "Softmax":
                 x = vals[self.t(n["inputs"][0])]
                 vals[nid] = torch.softmax(x, dim=-1)
+            if timeline is not None:
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1.record()
+                timeline.append((nid, st.kind, ev0, ev1))
             last = self.t(nid)
             release(n)
         out = vals[last]

@@ -1,9 +1,11 @@
-"""bench.py's reference arm runs on CPU: check its JSON line against the driver contract."""
+"""bench.py JSON lines against the driver contract: the reference arm on CPU, the product arm on the GPU."""
 
 import json
 import subprocess
 import sys
 from pathlib import Path
+
+import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
 
@@ -21,3 +23,20 @@ def test_reference_arm_json_line():
     assert line["e2e"] == {"value": line["value"], "unit": "GMAC/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert "ResNet-8" in line["config"]["workload"] and line["config"]["batch_per_gpu"] == 1024
+
+
+@pytest.mark.gpu
+def test_b200_arm_json_line():
+    """The product arm's line carries every contract key with the right types (a short run)."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--cpu-budget", "0.5"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["unit"] == "GMAC/s" and line["value"] > 0 and line["n_gpus"] == 1 and line["steps"] == 3
+    assert isinstance(line["gpu_launches"], int) and line["gpu_launches"] > 0
+    roof = line["roofline"]
+    assert 0 < roof["frac"] <= 1 and roof["achieved"] > 0 and roof["peak"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+    assert line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["cores"] >= 1
+    assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}

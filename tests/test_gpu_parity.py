@@ -731,3 +731,46 @@ def test_ftable_kernel_long_k_packed_sums_exact(mode):
         assert kern.startswith("ft"), kern
         assert bits_equal(y, want), kern
         assert np.array_equal(acc, want_acc), kern
+
+
+def test_run_benchmark_report_and_outputs(tmp_path):
+    """benchmark.run_benchmark (reference bench.py:37-87 on the GPU engine): outputs bit-identical to the
+    reference executor's for a reference model file; report phases partition t_init + t_comp; MAC count
+    = graph MACs x images; CIFAR-10 files run through the on-device record decode."""
+    from paper_2002_09481_b200 import formats as F
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.benchmark import run_benchmark, speedup
+    from paper_2002_09481_b200.datasets import synthetic_cifar10
+
+    g = load_golden("formats")
+    (tmp_path / "ax.json").write_bytes(g["model_json"].tobytes())
+    (tmp_path / "ax.weights.bin").write_bytes(g["model_weights"].tobytes())
+    F.save_lut(T.truncated_lut(T.Signedness.SIGNED, 2), tmp_path / "ax.axm")
+    x = g["model_input"]
+    # one range-batch = the reference executor's batch (ranges are per batch, graph.py:270-275)
+    report, out = run_benchmark(tmp_path / "ax.json", x, batch_size=x.shape[0])
+    assert bits_equal(out, g["model_logits"])
+    assert report.t_init > 0 and report.t_comp > 0 and report.phase_seconds["lut_lookup"] > 0
+    assert abs(sum(report.phase_seconds.values()) - report.total) <= 1e-9 * max(1.0, report.total)
+    assert report.mac_count > 0 and report.per_layer
+    F.save_report(report, tmp_path / "r.json")
+    back = F.load_report(tmp_path / "r.json")
+    assert back.mac_count == report.mac_count and back.phase_seconds == report.phase_seconds
+    assert F.report_csv(back).startswith("name,seconds,percent\nlut_lookup,")
+    assert speedup(report, report) == 1.0
+
+    lut = T.truncated_lut(T.Signedness.SIGNED, 2)
+    nodes = resnet.cifar_resnet(1, lut, seed=0)
+    imgs, labels = synthetic_cifar10(200, seed=5)
+    F.save_cifar10(tmp_path / "data.bin", imgs, labels)
+    rep_f, out_f = run_benchmark(nodes, tmp_path / "data.bin", batch_size=64)
+    rep_a, out_a = run_benchmark(nodes, imgs, batch_size=64, batches=4)
+    assert out_f.shape[0] == 200 and bits_equal(out_f, out_a)
+    assert rep_f.mac_count == rep_a.mac_count == 200 * _graph_macs(nodes)
+
+
+def _graph_macs(nodes):
+    from oracle.axemu_oracle import graph_mac_count
+
+    return graph_mac_count(nodes, (1, 32, 32, 3))
