@@ -82,9 +82,9 @@ def workload_spec(name: str, lut_kind: str):
 
 
 def lib_variant_name(v: int) -> str:
-    from paper_2002_09481_b200 import _lib
+    from paper_2002_09481_b200.graph import variant_name
 
-    return _lib.load().axb_ft_variant_name(int(v)).decode() if v else "auto"
+    return variant_name(int(v))
 
 
 def sweep_luts():

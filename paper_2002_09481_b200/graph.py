@@ -80,7 +80,7 @@ class _ConvPlan:
     out_shape: tuple = ()
     pads: tuple = ()
     layer: ConvLayer | None = None
-    ft_variant: int = 0         # ftable-kernel tile variant (0 = cost model; set by autotune)
+    ft_variant: int = 0         # ftable-kernel tile variant (0 = cost model; -1 = b-major LUT kernel; autotune)
 
 
 @dataclass
@@ -381,9 +381,10 @@ class GpuGraph:
         return out
 
     def autotune(self, batch: torch.Tensor, reps: int = 3) -> dict:
-        """Pick each conv layer's ftable-kernel variant by timing every variant on the layer's
-        real input (one pass over ``batch``; like a cuDNN benchmark mode).  All variants must
-        produce identical bits -- checked here, on live data.  Returns {node id: variant name}."""
+        """Pick each conv layer's kernel by timing every ftable-kernel variant and the b-major LUT
+        kernel (``lutconv_fast``; fewer bank conflicts on high-entropy codes) on the layer's real
+        input (one pass over ``batch``; like a cuDNN benchmark mode).  All candidates must produce
+        identical bits -- checked here, on live data.  Returns {node id: kernel name}."""
         self._tune = max(1, int(reps))
         try:
             self.run(batch)
@@ -392,11 +393,11 @@ class GpuGraph:
         names = {}
         for st in self.steps:
             if st.kind == "conv" and st.plan.ft_variant:
-                names[st.node["id"]] = self.lib.axb_ft_variant_name(st.plan.ft_variant).decode()
+                names[st.node["id"]] = variant_name(st.plan.ft_variant)
         return names
 
     def tuning(self) -> dict:
-        """{conv node id: ftable variant index} (0 = cost model)."""
+        """{conv node id: kernel choice} (ftable variant index; 0 = cost model, -1 = b-major LUT kernel)."""
         return {st.node["id"]: st.plan.ft_variant for st in self.steps if st.kind == "conv"}
 
     def set_tuning(self, picks: dict) -> None:
@@ -534,11 +535,11 @@ class GpuGraph:
         if self._tune and p.layer.ftable is not None and not self.variant:
             # re-running the layer is idempotent: same codes, same outputs, same range / flag bits
             best, best_t, ref = 0, float("inf"), None
-            for v in range(1, self.lib.axb_ft_variant_count()):
+            for v in list(range(1, self.lib.axb_ft_variant_count())) + [-1]:
                 evs = []
                 for _ in range(self._tune):
                     pr = []
-                    y = p.layer.run(x, in_rng, ft_variant=v, profile=pr, **kw)
+                    y = p.layer.run(x, in_rng, ft_variant=max(v, 0), use_ftable=v >= 0, profile=pr, **kw)
                     evs.append(pr[0])
                 torch.cuda.synchronize(self.device)
                 t = sorted(a.elapsed_time(b) for a, b, *_ in evs)[len(evs) // 2]
@@ -546,17 +547,25 @@ class GpuGraph:
                     ref = y
                 elif not torch.equal(ref.view(torch.int32), y.view(torch.int32)):
                     bad = (ref.view(torch.int32) != y.view(torch.int32)).reshape(-1).nonzero()
-                    raise _lib.AxbError(f"ftable variant {v} changed the bits of {p.node['id']!r}: {bad.numel()} of "
+                    raise _lib.AxbError(f"kernel {variant_name(v)} changed the bits of {p.node['id']!r}: {bad.numel()} of "
                                         f"{y.numel()} outputs, first flat indices {bad[:4, 0].tolist()}, shape "
                                         f"{tuple(y.shape)}")
                 if t < best_t:
                     best, best_t = v, t
             p.ft_variant = best
-        out = p.layer.run(x, in_rng, profile=prof, ft_variant=p.ft_variant, **kw)
+        out = p.layer.run(x, in_rng, profile=prof, ft_variant=max(p.ft_variant, 0), use_ftable=p.ft_variant >= 0,
+                          **kw)
         if prof:
             self._profile.append((p.node["id"],) + prof[0])
         self.launches += p.layer.launches
         return out
+
+
+def variant_name(v: int) -> str:
+    """Name of a per-layer kernel choice (``GpuGraph.tuning()`` values)."""
+    if v < 0:
+        return "lut_bmajor"
+    return _lib.load().axb_ft_variant_name(int(v)).decode() if v else "auto"
 
 
 def run(nodes, batch, **kw) -> torch.Tensor:

@@ -581,8 +581,9 @@ def test_fused_quantize_im2col_equals_two_pass(mode):
 
 
 def test_graph_autotune_keeps_bits():
-    """Per-layer kernel autotune (every ftable variant timed on live activations, bits compared
-    inside) leaves the logits bit-identical to the cost-model run and to the oracle graph."""
+    """Per-layer kernel autotune (every ftable variant and the b-major LUT kernel timed on live
+    activations, bits compared inside) leaves the logits bit-identical to the cost-model run; a
+    forced LUT-kernel pick (tuning value -1) runs that kernel with the same bits."""
     torch = _torch()
     from paper_2002_09481_b200 import resnet
     from paper_2002_09481_b200 import types as T
@@ -594,8 +595,12 @@ def test_graph_autotune_keeps_bits():
     x = torch.from_numpy(imgs).cuda()
     want = g.run(x).cpu().numpy()
     picks = g.autotune(x, reps=1)
-    assert len(picks) == 10 and all(v.startswith("ft") for v in picks.values()), picks
+    assert len(picks) == 10 and all(v.startswith("ft") or v == "lut_bmajor" for v in picks.values()), picks
     assert bits_equal(g.run(x).cpu().numpy(), want)
+    g.set_tuning({nid: -1 for nid in g.tuning()})
+    prof = []
+    assert bits_equal(g.run(x, profile=prof).cpu().numpy(), want)
+    assert {fam for *_, fam in prof} == {"lutconv_fast"}, {fam for *_, fam in prof}
 
 
 def test_operator_api_large_call_uses_ftable_bit_exact():
