@@ -105,29 +105,43 @@ __global__ void __launch_bounds__(256) pool4_kernel(const float4 *__restrict__ x
         const int oy = (int)(t2 - b * (uint32_t)oh);
         float r[4];
         int valid = 0;
-        bool first = true;
 #pragma unroll
         for (int j = 0; j < 4; ++j) r[j] = MAX ? -INFINITY : 0.0f;
-        for (int ky = 0; ky < ph; ++ky) {
-            const int iy = oy * sh + ky - pt;
-            for (int kx = 0; kx < pw; ++kx) {
-                const int ix = ox * sw + kx - pl;
-                const bool in = iy >= 0 && iy < h && ix >= 0 && ix < w;
-                float4 v4 = make_float4(MAX ? -INFINITY : 0.0f, MAX ? -INFINITY : 0.0f, MAX ? -INFINITY : 0.0f,
-                                        MAX ? -INFINITY : 0.0f);
-                if (in) v4 = __ldg(x + (((int64_t)b * h + iy) * w + ix) * c4 + cg);
-                const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+        // taps in sequential (ky, kx) order, PB at a time: the PB loads are issued before the
+        // dependent fp32 chain consumes them (a global 8x8 pool has only n*c/4 threads, so memory-
+        // level parallelism per thread is what bounds it); the arithmetic order is unchanged
+        constexpr int PB = 16;
+        const int taps = ph * pw;
+        int ky = 0, kx = 0;
+        for (int t0 = 0; t0 < taps; t0 += PB) {
+            float4 vv[PB];
+            bool inb[PB];
+#pragma unroll
+            for (int u = 0; u < PB; ++u) {
+                const int iy = oy * sh + ky - pt, ix = ox * sw + kx - pl;
+                inb[u] = t0 + u < taps && iy >= 0 && iy < h && ix >= 0 && ix < w;
+                vv[u] = make_float4(MAX ? -INFINITY : 0.0f, MAX ? -INFINITY : 0.0f, MAX ? -INFINITY : 0.0f,
+                                    MAX ? -INFINITY : 0.0f);
+                if (inb[u]) vv[u] = __ldg(x + (((int64_t)b * h + iy) * w + ix) * c4 + cg);
+                if (++kx == pw) {
+                    kx = 0;
+                    ++ky;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PB; ++u) {
+                if (t0 + u >= taps) break;
+                const float v[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     if (MAX) {
                         if (r[j] == r[j] && (v[j] > r[j] || v[j] != v[j])) r[j] = v[j];  // np.max, NaN wins
                     } else {
-                        const float u = v[j] != v[j] ? 0.0f : v[j];  // nansum
-                        r[j] = first ? u : __fadd_rn(r[j], u);
+                        const float q = v[j] != v[j] ? 0.0f : v[j];  // nansum
+                        r[j] = (t0 + u == 0) ? q : __fadd_rn(r[j], q);
                     }
                 }
-                valid += in;
-                first = false;
+                valid += inb[u];
             }
         }
         if (!MAX) {
@@ -211,6 +225,16 @@ static int grid_for(int64_t total) {
     return blocks < 1 ? 1 : (int)blocks;
 }
 
+// Small pools (e.g. the global 8x8 average pool: n*c/4 threads, each a long tap chain): 64-thread
+// blocks so every SM gets work.
+static void pool_launch_dims(uint32_t t4, int *grid, int *block) {
+    *block = t4 < (uint32_t)sm_count() * 4 * 256 ? 64 : 256;
+    int64_t blocks = ((int64_t)t4 + *block - 1) / *block;
+    const int64_t cap = (int64_t)sm_count() * 16 * (256 / *block);
+    if (blocks > cap) blocks = cap;
+    *grid = blocks < 1 ? 1 : (int)blocks;
+}
+
 }  // namespace axb
 
 using namespace axb;
@@ -272,7 +296,9 @@ int axb_maxpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, in
     if (c % 4 == 0 && total / 4 < (int64_t(1) << 32) && ((reinterpret_cast<uintptr_t>(d_x) |
                                                             reinterpret_cast<uintptr_t>(d_out)) & 15) == 0) {
         const uint32_t t4 = (uint32_t)(total / 4);
-        pool4_kernel<true><<<grid_for(t4), 256, 0, (cudaStream_t)stream>>>(
+        int pg, pb;
+        pool_launch_dims(t4, &pg, &pb);
+        pool4_kernel<true><<<pg, pb, 0, (cudaStream_t)stream>>>(
             reinterpret_cast<const float4 *>(d_x), (int)h, (int)w, (int)(c / 4), ph, pw, sh, sw, pt, pl, (int)oh,
             (int)ow, t4, make_fastdiv((uint32_t)(c / 4)), make_fastdiv((uint32_t)ow), make_fastdiv((uint32_t)oh),
             reinterpret_cast<float4 *>(d_out), d_out_range, d_flags);
@@ -291,7 +317,9 @@ int axb_avgpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, in
     if (c % 4 == 0 && total / 4 < (int64_t(1) << 32) && ((reinterpret_cast<uintptr_t>(d_x) |
                                                             reinterpret_cast<uintptr_t>(d_out)) & 15) == 0) {
         const uint32_t t4 = (uint32_t)(total / 4);
-        pool4_kernel<false><<<grid_for(t4), 256, 0, (cudaStream_t)stream>>>(
+        int pg, pb;
+        pool_launch_dims(t4, &pg, &pb);
+        pool4_kernel<false><<<pg, pb, 0, (cudaStream_t)stream>>>(
             reinterpret_cast<const float4 *>(d_x), (int)h, (int)w, (int)(c / 4), ph, pw, sh, sw, pt, pl, (int)oh,
             (int)ow, t4, make_fastdiv((uint32_t)(c / 4)), make_fastdiv((uint32_t)ow), make_fastdiv((uint32_t)oh),
             reinterpret_cast<float4 *>(d_out), d_out_range, d_flags);
