@@ -81,6 +81,8 @@ class _ConvPlan:
     pads: tuple = ()
     layer: ConvLayer | None = None
     ft_variant: int = 0         # ftable-kernel tile variant (0 = cost model; -1 = b-major LUT kernel; autotune)
+    share_from: str | None = None  # conv node whose code tensor of the same input this 1x1 layer reads
+    exports: bool = False          # another conv reads this layer's code tensor
 
 
 @dataclass
@@ -245,6 +247,23 @@ class GpuGraph:
             elif st.kind == "Softmax":
                 shapes[n["id"]] = shapes[self.t(n["inputs"][0])]
         self.shapes = shapes
+        # quantize once per tensor: a later 1x1 unpadded conv of the same input (a ResNet projection next
+        # to the block's first conv) reads the earlier conv's zp-padded code tensor
+        first: dict[str, _ConvPlan] = {}
+        for st in self.steps:
+            if st.kind != "conv":
+                continue
+            p = st.plan
+            p.share_from, p.exports = None, False
+            tid = self.t(p.x)
+            a = first.get(tid)
+            if a is None:
+                if not p.layer.kp and not p.layer.depthwise:
+                    first[tid] = p
+                continue
+            _, h, w, _ = p.in_shape
+            if p.layer.shares_codes_with(a.layer) and resolve_padding(p.geometry, h, w, 1, 1) == (0, 0, 0, 0):
+                p.share_from, a.exports = a.node["id"], True
         self._prepared_for = tuple(in_shape)
 
     # ------------------------------------------------------------------ execution
@@ -276,6 +295,7 @@ class GpuGraph:
         self.flags.zero_()
         self.launches = 0  # libaxb kernels launched by this run
         self._profile = profile
+        self._codes: dict[str, dict] = {}  # exported code tensors (share_from), alive for this run
         vals: dict[str, torch.Tensor] = {}
         remaining = {tid: 0 for tid in self.slot}
         for n in self.nodes:
@@ -531,6 +551,8 @@ class GpuGraph:
         prof = [] if self._profile is not None else None
         kw = dict(relu=p.relu, residual=res, out_range=out_range, out_flag=out_flag,
                   quant_flag=self.flags[len(self.slot)].data_ptr(), sm_limit=self.sm_limit, variant=self.variant)
+        shared = self._codes.get(p.share_from) if p.share_from and not self.variant else None
+        codes_out = {} if p.exports else None
         in_rng = self.ranges[self.slot[self.t(p.x)]].data_ptr()
         if self._tune and p.layer.ftable is not None and not self.variant:
             # re-running the layer is idempotent: same codes, same outputs, same range / flag bits
@@ -539,7 +561,8 @@ class GpuGraph:
                 evs = []
                 for _ in range(self._tune):
                     pr = []
-                    y = p.layer.run(x, in_rng, ft_variant=max(v, 0), use_ftable=v >= 0, profile=pr, **kw)
+                    y = p.layer.run(x, in_rng, ft_variant=max(v, 0), use_ftable=v >= 0, profile=pr,
+                                    codes_in=shared if v >= 0 else None, **kw)
                     evs.append(pr[0])
                 torch.cuda.synchronize(self.device)
                 t = sorted(a.elapsed_time(b) for a, b, *_ in evs)[len(evs) // 2]
@@ -554,7 +577,9 @@ class GpuGraph:
                     best, best_t = v, t
             p.ft_variant = best
         out = p.layer.run(x, in_rng, profile=prof, ft_variant=max(p.ft_variant, 0), use_ftable=p.ft_variant >= 0,
-                          **kw)
+                          codes_in=shared if p.ft_variant >= 0 else None, codes_out=codes_out, **kw)
+        if codes_out:
+            self._codes[p.node["id"]] = codes_out
         if prof:
             self._profile.append((p.node["id"],) + prof[0])
         self.launches += p.layer.launches

@@ -88,6 +88,15 @@ class ConvLayer:
                                               self.lut.handle, self.ftable.data_ptr(), stream))
         self.launches = 0
 
+    def shares_codes_with(self, other: "ConvLayer") -> bool:
+        """True when this layer can read ``other``'s code tensor of the same input instead of quantizing
+        it again: a 1x1 layer without padding on the ftable kernel, same channels, signedness and rounding
+        (same range -> identical codes and coefficients; quantizer.py:98-131)."""
+        return (self.kh == self.kw == 1 and not self.kp and not self.depthwise and not other.kp
+                and not other.depthwise and self.ftable is not None and self.cin == other.cin
+                and self.sgn == other.sgn and self.round == other.round
+                and tuple(self.geometry.dilations) == (1, 1))
+
     def set_input_params(self, mn: float, mx: float) -> None:
         """Host range (the operator-API path): coefficients computed on the host, uploaded."""
         hp = _lib.QParams()
@@ -97,9 +106,15 @@ class ConvLayer:
 
     def run(self, x: torch.Tensor, in_range_dev=None, *, relu=False, residual=None, out_range=None,
             out_flag=None, quant_flag=None, acc_out=None, force_generic=False, sm_limit=0, variant=0,
-            pixel_order=0, profile=None, ft_variant=0, use_ftable=True) -> torch.Tensor:
+            pixel_order=0, profile=None, ft_variant=0, use_ftable=True, codes_in=None,
+            codes_out=None) -> torch.Tensor:
         """x: (n,h,w,cin) fp32 CUDA.  in_range_dev: device int32[2] ordered-float range, or None if
-        set_input_params() was called.  Returns (n,oh,ow,cout) fp32."""
+        set_input_params() was called.  Returns (n,oh,ow,cout) fp32.
+
+        ``codes_out`` (a dict) receives this call's zp-padded code tensor and its quantization
+        parameters; ``codes_in`` (such a dict, from another layer quantizing the SAME tensor with the
+        same range, signedness and rounding) lets a 1x1 unpadded layer on the ftable kernel skip its
+        own quantize pass and read the interior of that tensor (``shares_codes_with``)."""
         lib = self.lib
         n, h, w, c = (int(v) for v in x.shape)
         if c != (self.cout if self.depthwise else self.cin):
@@ -129,6 +144,16 @@ class ConvLayer:
             self.launches += 1
             d.n, d.hp, d.wp, d.cs, d.c = n, oh, ow, self.kp, self.kh * self.kw * c
             d.kh = d.kw = d.sh = d.sw = d.dh = d.dw = 1
+        elif codes_in is not None:  # read another layer's code tensor: interior pixel (y, x) at (y+pt, x+pl)
+            if not (self.ftable is not None and use_ftable and not variant and not force_generic
+                    and (pt, pb, pl, pr) == (0, 0, 0, 0) and self.kh == self.kw == 1 and codes_in["cs"] == in_cs
+                    and codes_in["n"] == n and codes_in["h"] == h and codes_in["w"] == w):
+                raise ValueError("shared code tensor does not fit this layer")
+            codes, pixsum = codes_in["codes"], None
+            d.n, d.hp, d.wp, d.cs, d.c = n, codes_in["hp"], codes_in["wp"], in_cs, c
+            d.kh = d.kw = 1
+            d.sh, d.sw = g.strides
+            d.dh, d.dw = g.dilations
         else:
             codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
             # the ftable kernel sums patch codes in its loop; only the LUT / generic kernels read pixsum
@@ -148,11 +173,17 @@ class ConvLayer:
             d.kh, d.kw = self.kh, self.kw
             d.sh, d.sw = g.strides
             d.dh, d.dw = g.dilations
+            if codes_out is not None:
+                codes_out.update(codes=codes, n=n, h=h, w=w, hp=hp_, wp=wp_, pt=pt, pl=pl, cs=in_cs,
+                                 params=self.params[0])
         d.codes, d.pixsum = codes.data_ptr(), (pixsum.data_ptr() if pixsum is not None else None)
+        if codes_in is not None:
+            d.codes += (codes_in["pt"] * codes_in["wp"] + codes_in["pl"]) * in_cs
         d.oh, d.ow = oh, ow
         d.fcodes, d.fsum = self.fcodes.data_ptr(), self.fsum.data_ptr()
         d.cout, d.coutp, d.kpad = self.cout, self.coutp, self.kpad
-        d.in_params, d.f_params = self.params[0].data_ptr(), self.params[1].data_ptr()
+        d.in_params = (codes_in["params"] if codes_in is not None else self.params[0]).data_ptr()
+        d.f_params = self.params[1].data_ptr()
         d.accumulator = self.acc
         d.relu = int(relu)
         d.bias = self.bias.data_ptr() if self.bias is not None else None

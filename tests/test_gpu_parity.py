@@ -779,3 +779,24 @@ def _graph_macs(nodes):
     from oracle.axemu_oracle import graph_mac_count
 
     return graph_mac_count(nodes, (1, 32, 32, 3))
+
+
+def test_projection_reads_first_conv_codes():
+    """A ResNet projection (1x1, unpadded, same input as the block's first conv) reads that conv's
+    zp-padded code tensor instead of quantizing again: one quantize launch fewer per projection, and
+    the logits stay bit-identical to the reference executor's (the projections host the fused
+    residual Add + ReLU, so their own values are covered through the logits)."""
+    torch = _torch()
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    g = load_golden("nets")
+    gg = GpuGraph(resnet.cifar_resnet(1, T.truncated_lut(T.Signedness.SIGNED, 2), seed=0))
+    y = gg.run(torch.from_numpy(g["r8_trunc2_x"]).cuda()).cpu().numpy()
+    shared = {nid: p.share_from for nid, p in gg.conv_plans.items() if p.share_from}
+    assert shared == {"s1b0.proj": "s1b0.a", "s2b0.proj": "s2b0.a"}, shared
+    assert bits_equal(y, g["r8_trunc2_logits"])
+    prof = []
+    gg.run(torch.from_numpy(g["r8_trunc2_x"]).cuda(), profile=prof)
+    assert gg.launches == 1 + 10 + 10 - 2 + 1  # input range, 10 convs, 10 quantizes minus 2 shared, pool
