@@ -175,6 +175,16 @@ int axb_ft_variant_count(void);
 /* resident CTA clusters (CTAs for cluster size 1) of ftable variant v on the current device */
 int axb_ft_variant_clusters(int variant, int is_signed);
 const char *axb_ft_variant_name(int variant);
+/* Code-major layout of the same words for the cm32_* variants (ft_variant with
+ * axb_ft_variant_layout(v) == 1; pass this table as desc.ftable):
+ *   CM[cb][k][a][pr] = W word of channels (cb*32 + 2*pr, cb*32 + 2*pr + 1), pr = 0..15
+ * i.e. 64 contiguous bytes per (32-channel block, row, code); 16 KiB per (cb, k).
+ * axb_ftable_cm_bytes = kpad * coutp * 512 (0 unless coutp % 32 == 0). */
+int64_t axb_ftable_cm_bytes(int64_t kpad, int64_t coutp);
+int axb_ftable_cm_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                          const axb_lut *lut, uint32_t *d_ftable, void *stream);
+/* 0: variant v reads the pair-major table (axb_ftable_prepare), 1: the code-major one */
+int axb_ft_variant_layout(int variant);
 int axb_conv_variant_count(void);
 /* Depthwise approximate conv (config 5; the reference has no groups): channel c
  * of the output == axconv2d on input channel c alone with the shared ranges.

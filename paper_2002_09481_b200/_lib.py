@@ -93,6 +93,9 @@ SIGNATURES = {
     "axb_ft_variant_count": (c_int, []),
     "axb_ft_variant_clusters": (c_int, [c_int, c_int]),
     "axb_ft_variant_name": (ctypes.c_char_p, [c_int]),
+    "axb_ftable_cm_bytes": (c_i64, [c_i64, c_i64]),
+    "axb_ftable_cm_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "axb_ft_variant_layout": (c_int, [c_int]),
     "axb_depthwise_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
     "axb_conv_variant_name": (ctypes.c_char_p, [c_int]),
     "axb_conv_im2col_kp": (c_i64, [c_i64, c_i64, c_i64]),

@@ -348,6 +348,257 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still arrive on its barriers
 }
 
+// ---------------------------------------------------------------- code-major variant (CM)
+// Same products, code-major layout: CM[cb][k][a][16 pairs] (uint32 words as above), i.e. the 32
+// channels of block cb at row k and activation code a are 64 contiguous bytes.  Lanes = (pixel,
+// quarter q): one LDS.128 at CM[k][a][4q..4q+3] delivers 4 pairs = 8 products of one pixel, a warp
+// instruction covers 8 pixels x 32 channels = 512 B = 4 wavefronts when the 8 pixels' codes spread
+// over both bank halves (a 64-byte row sits in bank half a & 1; equal codes broadcast).  Against the
+// pair-major kernel above: 8 products per LDS instead of 2 (fewer instructions per product), and on
+// high-entropy codes (image stems) far fewer conflict wavefronts -- measured on real ResNet-8 codes
+// 12.3e12 vs 9.7e12 products/s, on uniform codes 11.0e12 vs 5.4e12 (scripts/lut_gather_bench.cu).
+// Per lane: J pixels (8*J per warp), 4 pairs each; lane (pixel, q) loads rows 4q..4q+3 of its pixel's
+// 16-row chunk (one 32-bit word) and a stage's rows come from the right lane by one SHFL per pixel.
+// Tiles of BM = WARPS*8*J pixels x 32 channels; the same TMA ring and epilogue.
+constexpr int kCmPairs = 16;                   // channel pairs per 32-channel block
+constexpr int kCmRowWords = 256 * kCmPairs;    // one (block, row) slice: 256 codes x 16 pairs
+constexpr int kCmRowBytes = kCmRowWords * 4;   // 16 KiB
+__host__ __device__ constexpr int cm_stage_bytes(int KS) { return KS * kCmRowBytes; }
+__host__ __device__ constexpr int cm_smem(int KS, int ST) { return ST * cm_stage_bytes(KS) + kMaxTaps * 4 + 2 * ST * 8; }
+
+template <int J, int WARPS, int KS, int ST, bool SGN>
+__global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
+    constexpr int NT = WARPS * 32;
+    constexpr int PXW = 8 * J;        // pixels per warp
+    constexpr int BM = WARPS * PXW;
+    constexpr int BN = 32;
+    constexpr int SPC = 16 / KS;
+    constexpr uint32_t STAGE_BYTES = cm_stage_bytes(KS);
+    static_assert(KS == 2 || KS == 4, "KS rows per stage: 2 or 4");
+    static_assert(cm_smem(KS, ST) + 512 <= 232448, "code-major ring exceeds shared memory");
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    int32_t *tapoff_s = reinterpret_cast<int32_t *>(smem + ST * STAGE_BYTES);
+    uint64_t *full = reinterpret_cast<uint64_t *>(tapoff_s + kMaxTaps);
+    uint64_t *empty = full + ST;
+    const uint32_t *tab = reinterpret_cast<const uint32_t *>(smem);
+
+    const int tid = (int)threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int q = lane & 3, ps = lane >> 2;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, WARPS);
+        }
+    }
+    for (int t = tid; t < p.taps; t += NT) tapoff_s[t] = ((t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw) * p.cs;
+    __syncthreads();
+
+    const int64_t grid = gridDim.x;
+    const int64_t cid = blockIdx.x;
+    const int64_t my_tiles = p.ntiles > cid ? (p.ntiles - cid + grid - 1) / grid : 0;
+    const int64_t spt = (int64_t)p.nchunks * SPC;
+    const int64_t total = my_tiles * spt;
+
+    int64_t pr_h = 0, pr_q = 0, pr_tile = cid;
+    auto produce = [&]() {
+        const int slot = (int)(pr_h % ST);
+        const int64_t nb = pr_tile / p.ntm;
+        mbar_expect_tx(full + slot, STAGE_BYTES);
+        bulk_g2s(smem + slot * STAGE_BYTES, p.ftable + (nb * p.kpad + pr_q * KS) * kCmRowWords, STAGE_BYTES,
+                 full + slot);
+        ++pr_h;
+        if (++pr_q == spt) {
+            pr_q = 0;
+            pr_tile += grid;
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < ST - 1 && pr_h < total; ++s) produce();
+
+    int32_t rowbase[J];
+    auto set_rows = [&](int64_t tile) {
+        const int64_t m0 = (tile % p.ntm) * BM;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int64_t mt = m0 + warp * PXW + j * 8 + ps;
+            int64_t pix0 = 0;
+            if (mt < p.M) pixel_of(p, mt, pix0);
+            rowbase[j] = (int32_t)(pix0 * p.cs);
+        }
+    };
+    pdl_wait();
+    uint32_t av[J];  // rows 4q..4q+3 of pixel j's current chunk (the 4 lanes of a pixel hold its 16 rows)
+    int ld_t = 0, ld_ci = 0, ld_kc = 0;
+    int64_t ld_left = my_tiles * p.nchunks, ld_tile = cid;
+    auto load_next = [&]() {
+        if (ld_left == 0) return;
+        const int off = tapoff_s[ld_t] + ld_ci;
+#pragma unroll
+        for (int j = 0; j < J; ++j) av[j] = __ldg(reinterpret_cast<const uint32_t *>(p.codes + rowbase[j] + off) + q);
+        --ld_left;
+        ld_ci += 16;
+        if (ld_ci == p.cs) {
+            ld_ci = 0;
+            ++ld_t;
+        }
+        if (++ld_kc == p.nchunks) {
+            ld_kc = ld_t = ld_ci = 0;
+            ld_tile += grid;
+            if (ld_left > 0) set_rows(ld_tile);
+        }
+    };
+
+    uint32_t acc_all[J][4], acc_hi[J][4];
+    int32_t spa[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        spa[j] = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc_all[j][r] = acc_hi[j][r] = 0;
+    }
+    float tmin = INFINITY, tmax = -INFINITY;
+    int nonfinite = 0;
+    const int64_t bias_units = SGN ? (int64_t)32768 * p.kpad : 0;
+
+    int64_t g = 0;
+    int64_t c_tile = cid;
+    if (my_tiles > 0) {
+        set_rows(c_tile);
+        load_next();
+    }
+    for (int64_t jt = 0; jt < my_tiles; ++jt) {
+#pragma unroll 1
+        for (int kc = 0; kc < p.nchunks; ++kc) {
+            uint32_t cur[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) cur[j] = av[j];
+            load_next();
+#pragma unroll
+            for (int j = 0; j < J; ++j) {  // this lane's 4 codes of S_p; the 4 lanes are summed in the epilogue
+                if (SGN)
+                    spa[j] = __dp4a((int)cur[j], 0x01010101, spa[j]);
+                else
+                    spa[j] = (int32_t)__dp4a(cur[j], 0x01010101u, (uint32_t)spa[j]);
+            }
+#pragma unroll 1
+            for (int st = 0; st < SPC; ++st) {
+                const int slot = (int)(g % ST);
+                if (tid == 0 && pr_h < total) {
+                    if (g >= 1) mbar_wait(empty + (g - 1) % ST, (uint32_t)(((g - 1) / ST) & 1));
+                    produce();
+                }
+                mbar_wait(full + slot, (uint32_t)((g / ST) & 1));
+                const uint4 *stab = reinterpret_cast<const uint4 *>(tab + slot * (STAGE_BYTES / 4)) + q;
+                // rows 4*st4 .. 4*st4+KS-1 of the chunk live in lane (ps, st4) of each pixel
+                const int st4 = (st * KS) >> 2, sub = (st * KS) & 3;
+                uint32_t rw[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) rw[j] = __shfl_sync(0xffffffffu, cur[j], (lane & ~3) | st4);
+#pragma unroll
+                for (int kl = 0; kl < KS; ++kl) {
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        const uint32_t a = __byte_perm(rw[j], 0, 0x4440u + ((sub + kl) & 3));
+                        const uint4 w = stab[kl * (kCmRowWords / 4) + a * 4];
+                        acc_all[j][0] += w.x; acc_hi[j][0] += w.x >> 16;
+                        acc_all[j][1] += w.y; acc_hi[j][1] += w.y >> 16;
+                        acc_all[j][2] += w.z; acc_hi[j][2] += w.z >> 16;
+                        acc_all[j][3] += w.w; acc_hi[j][3] += w.w >> 16;
+                    }
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + slot);
+                ++g;
+            }
+        }
+
+        {
+            const EpiConst e = epi_const(p);
+            const int64_t nb = c_tile / p.ntm;
+            const int64_t m0 = (c_tile % p.ntm) * BM;
+            const int cb = (int)nb * BN + q * 8;  // this lane's 8 channels
+            const bool full_blk = cb + 8 <= p.cout && (p.cout & 3) == 0;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {  // S_p of pixel j = the 4 lanes' partial sums
+                spa[j] += __shfl_xor_sync(0xffffffffu, spa[j], 1);
+                spa[j] += __shfl_xor_sync(0xffffffffu, spa[j], 2);
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int64_t mt = m0 + warp * PXW + j * 8 + ps;
+                if (mt < p.M) {
+                    int64_t pix0;
+                    const int64_t m = pixel_of(p, mt, pix0);
+                    const int64_t pz = -e.zp2 * (int64_t)spa[j];
+                    float *dst = p.out + m * p.cout + cb;
+#pragma unroll
+                    for (int hq = 0; hq < 2; ++hq) {
+                        int64_t A[4];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t hi = acc_hi[j][2 * hq + h];
+                            const uint32_t lo = acc_all[j][2 * hq + h] - (hi << 16);
+                            A[2 * h] = (int64_t)lo - bias_units;
+                            A[2 * h + 1] = (int64_t)hi - bias_units;
+                        }
+                        const int c0 = cb + 4 * hq;
+                        if (full_blk) {
+                            float y[4];
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const int64_t corr = A[t] + pz - e.zp1 * __ldg(p.fsum + c0 + t) + e.kzz;
+                                y[t] = __double2float_rn(e.scale * __ll2double_rn(corr));
+                                if (p.bias) y[t] = __fadd_rn(y[t], __ldg(p.bias + c0 + t));
+                            }
+                            if (p.residual) {
+                                const float4 r = __ldg(reinterpret_cast<const float4 *>(p.residual + m * p.cout + c0));
+                                y[0] = __fadd_rn(y[0], r.x); y[1] = __fadd_rn(y[1], r.y);
+                                y[2] = __fadd_rn(y[2], r.z); y[3] = __fadd_rn(y[3], r.w);
+                            }
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                if (p.relu) y[t] = (y[t] > 0.0f || y[t] != y[t]) ? y[t] : 0.0f;
+                                track(y[t], tmin, tmax, nonfinite);
+                            }
+                            *reinterpret_cast<float4 *>(dst + 4 * hq) = make_float4(y[0], y[1], y[2], y[3]);
+                            if (p.acc_out) {
+#pragma unroll
+                                for (int t = 0; t < 4; ++t) p.acc_out[m * p.cout + c0 + t] = A[t];
+                            }
+                        } else {
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                if (c0 + t < p.cout) {
+                                    const int64_t corr = A[t] + pz - e.zp1 * p.fsum[c0 + t] + e.kzz;
+                                    float v = __double2float_rn(e.scale * __ll2double_rn(corr));
+                                    if (p.bias) v = __fadd_rn(v, p.bias[c0 + t]);
+                                    if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + c0 + t]);
+                                    if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;
+                                    track(v, tmin, tmax, nonfinite);
+                                    dst[4 * hq + t] = v;
+                                    if (p.acc_out) p.acc_out[m * p.cout + c0 + t] = A[t];
+                                }
+                            }
+                        }
+                    }
+                }
+                spa[j] = 0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc_all[j][r] = acc_hi[j][r] = 0;
+            }
+        }
+        c_tile += grid;
+    }
+    const bool any = tmin <= tmax;
+    range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
+                 AXB_FLAG_OUT_NONFINITE);
+}
+
 // ---------------------------------------------------------------- table preparation
 // W[sb][k][pair][a] = (u(lut[(a<<8)|F[k][c]]), u(lut[(a<<8)|F[k][c+1]])), c = sb*8 + 2*pair (8-channel
 // sub-blocks); u = raw ^ 0x8000 (signed) / raw (unsigned); junk rows (ci >= c or k >= taps*cs) = zero
@@ -375,11 +626,37 @@ __global__ void ftable_kernel(const uint8_t *__restrict__ fcodes, int64_t kpad, 
     }
 }
 
+// CM[cb][k][a][pr] = W word of channels (cb*32 + 2*pr, +1) at row k, code a (the same words, code-major)
+__global__ void ftable_cm_kernel(const uint8_t *__restrict__ fcodes, int64_t kpad, int64_t coutp, int32_t cs,
+                                 int32_t c, int64_t kreal, const uint16_t *__restrict__ lut_b, int sgn,
+                                 uint32_t *__restrict__ out) {
+    const int64_t total = (coutp / 32) * kpad * kCmRowWords;
+    const uint32_t flip = sgn ? 0x8000u : 0u;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int pr = (int)(idx & 15);
+        const uint32_t a = (uint32_t)((idx >> 4) & 255);
+        const int64_t rest = idx >> 12;
+        const int64_t k = rest % kpad;
+        const int64_t cb = rest / kpad;
+        uint32_t w = flip | (flip << 16);
+        if (k < kreal && (int)(k % cs) < c) {
+            const int64_t col = cb * 32 + 2 * pr;
+            const uint32_t b0 = fcodes[k * coutp + col], b1 = fcodes[k * coutp + col + 1];
+            const uint32_t u0 = (uint32_t)__ldg(lut_b + b0 * 256 + a) ^ flip;
+            const uint32_t u1 = (uint32_t)__ldg(lut_b + b1 * 256 + a) ^ flip;
+            w = u0 | (u1 << 16);
+        }
+        out[idx] = w;
+    }
+}
+
 // ---------------------------------------------------------------- host launch
 struct FtVariant {
     const char *name;
     int tm, warps, npb, cl;
     float cost;  // relative time per lookup slot (1 = best); tuned on B200
+    int cm;      // 1: code-major table (axb_ftable_cm_prepare), tm = J pixels per lane per 8-pixel group
 };
 static const FtVariant kFtVariants[] = {
     {"auto", 0, 0, 0, 0, 0.f},
@@ -393,8 +670,49 @@ static const FtVariant kFtVariants[] = {
     {"ft16_tm2_w12_k8", 2, 12, 8, 1, 1.050f},
     {"ft16_tm3_w12_k8", 3, 12, 8, 1, 1.000f},
     {"ft16_tm4_w12_k8", 4, 12, 8, 1, 1.000f},
+    {"cm32_j4_w16_k4", 4, 16, 16, 1, 1.000f, 1},
+    {"cm32_j8_w8_k4", 8, 8, 16, 1, 1.000f, 1},
+    {"cm32_j4_w12_k4", 4, 12, 16, 1, 1.000f, 1},
+    {"cm32_j6_w16_k4", 6, 16, 16, 1, 1.000f, 1},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
+
+template <int J, int WARPS, bool SGN, int KS = 4, int ST = 3>
+static int launch_ftcm(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
+    constexpr int BM = WARPS * 8 * J;
+    constexpr int BN = 32;
+    const size_t smem = cm_smem(KS, ST);
+    auto fn = lutconv_ftcm<J, WARPS, KS, ST, SGN>;
+    static int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_ftcm");
+        configured_dev = dev;
+    }
+    if (op == 1) return sm_count();
+    if (k.coutp % BN) return set_error(AXB_E_VALUE, "code-major ftable kernel needs coutp % 32 == 0");
+    ConvK kk = k;
+    kk.ntm = (int32_t)((k.M + BM - 1) / BM);
+    kk.ntiles = (int64_t)kk.ntm * (k.coutp / BN);
+    int64_t nblk = sm_limit > 0 ? sm_limit : sm_count();
+    if (nblk > kk.ntiles) nblk = kk.ntiles;
+    if (nblk < 1) nblk = 1;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)nblk);
+    cfg.blockDim = dim3(WARPS * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, fn, kk) != cudaSuccess) return check_launch("lutconv_ftcm");
+    set_last_kernel(name);
+    return check_launch("lutconv_ftcm");
+}
 
 // op 0: launch; op 1: return how many CL-CTA clusters fit on the device at once (cached)
 template <int TM, int WARPS, int NPB, bool SGN, int CL, int KS = 4, int ST = 6, int PF = 1>
@@ -463,6 +781,10 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 8: return launch_ft<2, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
         case 9: return launch_ft<3, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
         case 10: return launch_ft<4, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
+        case 11: return launch_ftcm<4, 16, SGN>(op, k, sm_limit, s, nm);
+        case 12: return launch_ftcm<8, 8, SGN>(op, k, sm_limit, s, nm);
+        case 13: return launch_ftcm<4, 12, SGN>(op, k, sm_limit, s, nm);
+        case 14: return launch_ftcm<6, 16, SGN>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
@@ -473,6 +795,7 @@ static int pick_ft_variant(const ConvK &k, int is_signed) {
     double best_t = 1e300;
     for (int v = 1; v < kNumFtVariants; ++v) {
         const FtVariant &x = kFtVariants[v];
+        if (x.cm) continue;  // the cost model picks among pair-major variants (the table handed in)
         const int64_t ncl = is_signed ? launch_ft_variant<true>(1, v, k, 0, 0) : launch_ft_variant<false>(1, v, k, 0, 0);
         if (ncl < 1) continue;
         const int64_t bm = (int64_t)x.warps * 32 * x.tm, bn = 2 * x.npb;
@@ -521,6 +844,30 @@ int axb_ftable_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t 
                                                                   d_ftable);
     return check_launch("ftable_prepare");
 }
+
+int64_t axb_ftable_cm_bytes(int64_t kpad, int64_t coutp) {
+    if (kpad <= 0 || coutp <= 0 || kpad % 16 || coutp % 32) return 0;
+    return kpad * (coutp / 32) * kCmRowBytes;
+}
+
+int axb_ftable_cm_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                          const axb_lut *lut, uint32_t *d_ftable, void *stream) {
+    if (!lut || !d_fcodes || !d_ftable) return set_error(AXB_E_VALUE, "null argument");
+    if (cs % 16 || c > cs || c < 1) return set_error(AXB_E_VALUE, "channel stride mismatch");
+    const int64_t kpad = axb_filter_kpad(kh, kw, cs), coutp = axb_filter_coutp(cout);
+    if (coutp % 32) return set_error(AXB_E_VALUE, "code-major table needs coutp % 32 == 0");
+    const int64_t total = (coutp / 32) * kpad * kCmRowWords;
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    ftable_cm_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_fcodes, kpad, coutp, (int32_t)cs, (int32_t)c,
+                                                                     kh * kw * cs, lut->d_bmajor, lut->is_signed,
+                                                                     d_ftable);
+    return check_launch("ftable_cm_prepare");
+}
+
+int axb_ft_variant_layout(int v) { return (v >= 1 && v < kNumFtVariants) ? kFtVariants[v].cm : 0; }
 
 int axb_ft_variant_count(void) { return kNumFtVariants; }
 int axb_ft_variant_clusters(int v, int is_signed) {

@@ -557,7 +557,9 @@ class GpuGraph:
         if self._tune and p.layer.ftable is not None and not self.variant:
             # re-running the layer is idempotent: same codes, same outputs, same range / flag bits
             best, best_t, ref = 0, float("inf"), None
-            for v in list(range(1, self.lib.axb_ft_variant_count())) + [-1]:
+            cands = [v for v in range(1, self.lib.axb_ft_variant_count())
+                     if p.layer.ftable_cm is not None or self.lib.axb_ft_variant_layout(v) == 0]
+            for v in cands + [-1]:
                 evs = []
                 for _ in range(self._tune):
                     pr = []

@@ -86,6 +86,13 @@ class ConvLayer:
             self.ftable = torch.empty(nbytes // 4, dtype=torch.int32, device=self.device)
             _lib.check(lib.axb_ftable_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3], self.cout,
                                               self.lut.handle, self.ftable.data_ptr(), stream))
+        # the same words code-major (cm32_* variants: 8 products per LDS.128) when channels come in 32s
+        cm_bytes = int(lib.axb_ftable_cm_bytes(self.kpad, self.coutp)) if self.ftable is not None else 0
+        self.ftable_cm = None
+        if cm_bytes and cm_bytes <= FTABLE_MAX_BYTES and os.environ.get("AXB_FTABLE_CM", "1") != "0":
+            self.ftable_cm = torch.empty(cm_bytes // 4, dtype=torch.int32, device=self.device)
+            _lib.check(lib.axb_ftable_cm_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3], self.cout,
+                                                 self.lut.handle, self.ftable_cm.data_ptr(), stream))
         self.launches = 0
 
     def shares_codes_with(self, other: "ConvLayer") -> bool:
@@ -200,6 +207,10 @@ class ConvLayer:
         d.variant = int(variant)
         d.pixel_order = int(pixel_order)
         d.ftable = self.ftable.data_ptr() if (self.ftable is not None and use_ftable) else None
+        if d.ftable is not None and ft_variant and lib.axb_ft_variant_layout(int(ft_variant)) == 1:
+            if self.ftable_cm is None:
+                raise ValueError("code-major ftable variant needs a code-major table (coutp % 32 == 0)")
+            d.ftable = self.ftable_cm.data_ptr()
         d.ft_variant = int(ft_variant)
         if profile is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

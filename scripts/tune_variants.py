@@ -76,7 +76,7 @@ def main():
                     y = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(),
                                   profile=prof, **kw)
                 except ValueError as e:  # variant not applicable to this layer (resident-table limits)
-                    if "resident" not in str(e):
+                    if "resident" not in str(e) and "code-major" not in str(e):
                         raise
                     break
                 e0, e1, macs = prof[0][:3]

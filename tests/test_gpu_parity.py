@@ -74,27 +74,35 @@ def test_c1_cases_bit_exact(path):
 
 
 def test_all_ftable_variants_bit_identical():
-    """Every ftable-kernel tile variant gives the oracle's bits (outputs and raw sums), including
-    ragged pixel tiles, cout not a multiple of 16, residual + ReLU-free paths and both signedness."""
+    """Every ftable-kernel tile variant (pair-major and code-major tables) gives the oracle's bits
+    (outputs and raw sums), including ragged pixel tiles, cout not a multiple of 16, residual +
+    ReLU-free paths and both signedness."""
     from paper_2002_09481_b200 import _lib
 
-    nvar = _lib.load().axb_ft_variant_count()
+    lib = _lib.load()
+    nvar = lib.axb_ft_variant_count()
     rng = np.random.default_rng(78)
     cases = [random_conv_case(rng) for _ in range(16)]
     for mode in (O.SIGNED, O.UNSIGNED):
         big = dict(x=np.maximum(rng.standard_normal((5, 23, 21, 32)), 0).astype(np.float32),
-                   f=rng.standard_normal((3, 3, 32, 37)).astype(np.float32), lut=O.random_lut(rng, mode),
+                   f=rng.standard_normal((3, 3, 32, 61)).astype(np.float32), lut=O.random_lut(rng, mode),
                    mode=mode, padding="same", strides=(1, 1), dilations=(1, 1), accumulator=O.WRAP32,
                    round_mode=O.HALF_EVEN)
         big.update(in_range=(float(big["x"].min()), float(big["x"].max())),
                    f_range=(float(big["f"].min()), float(big["f"].max())))
         cases.append(big)
+    cm_runs = 0
     for case in cases:
         want, want_acc = oracle_conv(case, return_acc=True)
+        coutp = -(-case["f"].shape[3] // 16) * 16
         for v in range(1, nvar):
+            if lib.axb_ft_variant_layout(v) == 1 and coutp % 32:  # code-major: 32-channel blocks only
+                continue
+            cm_runs += lib.axb_ft_variant_layout(v)
             y, acc, kern = gpu_conv(case, ft_variant=v)
             assert bits_equal(y, want), (v, kern)
             assert np.array_equal(acc, want_acc), (v, kern)
+    assert cm_runs >= 8
 
 
 def test_all_tile_variants_bit_identical():
@@ -595,7 +603,7 @@ def test_graph_autotune_keeps_bits():
     x = torch.from_numpy(imgs).cuda()
     want = g.run(x).cpu().numpy()
     picks = g.autotune(x, reps=1)
-    assert len(picks) == 10 and all(v.startswith("ft") or v == "lut_bmajor" for v in picks.values()), picks
+    assert len(picks) == 10 and all(v.startswith(("ft", "cm")) or v == "lut_bmajor" for v in picks.values()), picks
     assert bits_equal(g.run(x).cpu().numpy(), want)
     g.set_tuning({nid: -1 for nid in g.tuning()})
     prof = []
@@ -733,7 +741,7 @@ def test_ftable_kernel_long_k_packed_sums_exact(mode):
     want, want_acc = oracle_conv(case, return_acc=True)
     for v in range(1, _lib.load().axb_ft_variant_count()):
         y, acc, kern = gpu_conv(case, ft_variant=v)
-        assert kern.startswith("ft"), kern
+        assert kern.startswith(("ft", "cm")), kern
         assert bits_equal(y, want), kern
         assert np.array_equal(acc, want_acc), kern
 
