@@ -97,6 +97,48 @@ __global__ void __launch_bounds__(512, 1) bench_cm(const uint4 *__restrict__ cod
     if (s == 0x12345678u) out[0] = s;
 }
 
+// CM16: code-major with 16 channels per block (32 B per code): 2 lanes per pixel, 16 pixels per
+// LDS.128 instruction; a warp covers the group's 32 pixels in 2 instructions per tap.
+__global__ void __launch_bounds__(512, 1) bench_cm16(const uint4 *__restrict__ codes, int groups, uint32_t *out) {
+    constexpr int CM_ROWS = 4;              // 4 x 8 KiB rows
+    __shared__ __align__(16) uint32_t tab[CM_ROWS * 256 * 8];
+    for (int i = threadIdx.x; i < CM_ROWS * 256 * 8; i += blockDim.x) tab[i] = i * 2654435761u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, q = lane & 1, ps = lane >> 1;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    uint32_t all[2][4] = {}, hi[2][4] = {};
+    for (int rep = 0; rep < REPS; ++rep) {
+        for (int g = warp; g < groups; g += nwarps) {
+            uint32_t cw[2][4];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint4 c = __ldg(codes + g * 32 + j * 16 + ps);
+                cw[j][0] = c.x; cw[j][1] = c.y; cw[j][2] = c.z; cw[j][3] = c.w;
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint4 *row = reinterpret_cast<const uint4 *>(tab + (k % CM_ROWS) * 256 * 8) + q;
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t a = __byte_perm(cw[j][k >> 2], 0, 0x4440u + (k & 3));
+                    const uint4 w = row[a * 2];
+                    all[j][0] += w.x; hi[j][0] += w.x >> 16;
+                    all[j][1] += w.y; hi[j][1] += w.y >> 16;
+                    all[j][2] += w.z; hi[j][2] += w.z >> 16;
+                    all[j][3] += w.w; hi[j][3] += w.w >> 16;
+                }
+            }
+        }
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) s += all[j][p] ^ hi[j][p];
+    if (s == 0x12345678u) out[0] = s;
+}
+
 int main(int argc, char **argv) {
     const char *path = argc > 1 ? argv[1] : "build/codes_s0b0b.bin";
     FILE *f = fopen(path, "rb");
@@ -114,14 +156,15 @@ int main(int argc, char **argv) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     for (int i = 0; i < 5; ++i) bench<1><<<sms, 512>>>(d, groups, out);
     cudaDeviceSynchronize();
-    double best[3] = {0, 0, 0};
+    double best[4] = {0, 0, 0, 0};
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     for (int it = 0; it < 3; ++it) {
-        for (int w4 = 0; w4 < 3; ++w4) {
+        for (int w4 = 0; w4 < 4; ++w4) {
             cudaEventRecord(a);
-            if (w4 == 2) bench_cm<<<sms, 512>>>(d, groups, out);
+            if (w4 == 3) bench_cm16<<<sms, 512>>>(d, groups, out);
+            else if (w4 == 2) bench_cm<<<sms, 512>>>(d, groups, out);
             else if (w4) bench<1><<<sms, 512>>>(d, groups, out);
             else bench<0><<<sms, 512>>>(d, groups, out);
             cudaEventRecord(b);
@@ -134,7 +177,7 @@ int main(int argc, char **argv) {
         }
     }
     printf("{\"codes\": \"%s\", \"groups\": %d, \"W2_lds32_products_per_s\": %.4e, "
-           "\"W4_lds64_products_per_s\": %.4e, \"CM_lds128_products_per_s\": %.4e}\n", path, groups, best[0],
-           best[1], best[2]);
+           "\"W4_lds64_products_per_s\": %.4e, \"CM_lds128_products_per_s\": %.4e, \"CM16_lds128_products_per_s\": %.4e}\n",
+           path, groups, best[0], best[1], best[2], best[3]);
     return 0;
 }
