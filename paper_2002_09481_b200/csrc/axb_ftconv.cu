@@ -366,7 +366,7 @@ constexpr int kCmRowBytes = kCmRowWords * 4;   // 16 KiB
 __host__ __device__ constexpr int cm_stage_bytes(int KS) { return KS * kCmRowBytes; }
 __host__ __device__ constexpr int cm_smem(int KS, int ST) { return ST * cm_stage_bytes(KS) + kMaxTaps * 4 + 2 * ST * 8; }
 
-template <int J, int WARPS, int KS, int ST, bool SGN>
+template <int J, int WARPS, int KS, int ST, bool SGN, int PF>
 __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
     constexpr int NT = WARPS * 32;
     constexpr int PXW = 8 * J;        // pixels per warp
@@ -431,14 +431,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
         }
     };
     pdl_wait();
-    uint32_t av[J];  // rows 4q..4q+3 of pixel j's current chunk (the 4 lanes of a pixel hold its 16 rows)
+    uint32_t av[PF][J];  // rows 4q..4q+3 of pixel j's next chunks (the 4 lanes of a pixel hold its 16 rows)
     int ld_t = 0, ld_ci = 0, ld_kc = 0;
     int64_t ld_left = my_tiles * p.nchunks, ld_tile = cid;
-    auto load_next = [&]() {
+    auto load_next = [&](uint32_t(&dst)[J]) {
         if (ld_left == 0) return;
         const int off = tapoff_s[ld_t] + ld_ci;
 #pragma unroll
-        for (int j = 0; j < J; ++j) av[j] = __ldg(reinterpret_cast<const uint32_t *>(p.codes + rowbase[j] + off) + q);
+        for (int j = 0; j < J; ++j) dst[j] = __ldg(reinterpret_cast<const uint32_t *>(p.codes + rowbase[j] + off) + q);
         --ld_left;
         ld_ci += 16;
         if (ld_ci == p.cs) {
@@ -468,15 +468,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
     int64_t c_tile = cid;
     if (my_tiles > 0) {
         set_rows(c_tile);
-        load_next();
+#pragma unroll
+        for (int f = 0; f < PF; ++f) load_next(av[f]);
     }
     for (int64_t jt = 0; jt < my_tiles; ++jt) {
 #pragma unroll 1
         for (int kc = 0; kc < p.nchunks; ++kc) {
             uint32_t cur[J];
 #pragma unroll
-            for (int j = 0; j < J; ++j) cur[j] = av[j];
-            load_next();
+            for (int j = 0; j < J; ++j) {
+                cur[j] = av[0][j];
+                if (PF == 2) av[0][j] = av[1][j];
+            }
+            load_next(av[PF - 1]);
 #pragma unroll
             for (int j = 0; j < J; ++j) {  // this lane's 4 codes of S_p; the 4 lanes are summed in the epilogue
                 if (SGN)
@@ -677,12 +681,12 @@ static const FtVariant kFtVariants[] = {
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
-template <int J, int WARPS, bool SGN, int KS = 4, int ST = 3>
+template <int J, int WARPS, bool SGN, int PF = 1, int KS = 4, int ST = 3>
 static int launch_ftcm(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WARPS * 8 * J;
     constexpr int BN = 32;
     const size_t smem = cm_smem(KS, ST);
-    auto fn = lutconv_ftcm<J, WARPS, KS, ST, SGN>;
+    auto fn = lutconv_ftcm<J, WARPS, KS, ST, SGN, PF>;
     static int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -781,7 +785,7 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 8: return launch_ft<2, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
         case 9: return launch_ft<3, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
         case 10: return launch_ft<4, 12, 8, SGN, 1, 8, 3>(op, k, sm_limit, s, nm);
-        case 11: return launch_ftcm<4, 16, SGN>(op, k, sm_limit, s, nm);
+        case 11: return launch_ftcm<4, 16, SGN, 2>(op, k, sm_limit, s, nm);  // codes 2 chunks ahead
         case 12: return launch_ftcm<8, 8, SGN>(op, k, sm_limit, s, nm);
         case 13: return launch_ftcm<4, 12, SGN>(op, k, sm_limit, s, nm);
         case 14: return launch_ftcm<6, 16, SGN>(op, k, sm_limit, s, nm);
