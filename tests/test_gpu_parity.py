@@ -808,3 +808,33 @@ def test_projection_reads_first_conv_codes():
     prof = []
     gg.run(torch.from_numpy(g["r8_trunc2_x"]).cuda(), profile=prof)
     assert gg.launches == 1 + 10 + 10 - 2 + 1  # input range, 10 convs, 10 quantizes minus 2 shared, pool
+
+
+@pytest.mark.parametrize("mode", [O.SIGNED, O.UNSIGNED])
+def test_code_major_variants_vs_oracle(mode):
+    """The code-major kernel family (cm32_*: 32-channel blocks, LDS.128 of 4 pairs) over shapes the
+    pair-major test does not reach: cout 32 / 64 / 96 (one to three channel blocks, ragged 61), wide
+    and odd input channels, stride 2, dilation 2, ragged pixel tiles, every accumulator mode."""
+    from paper_2002_09481_b200 import _lib
+
+    lib = _lib.load()
+    cms = [v for v in range(1, lib.axb_ft_variant_count()) if lib.axb_ft_variant_layout(v) == 1]
+    assert len(cms) >= 3
+    rng = np.random.default_rng(4096 + (mode == O.SIGNED))
+    shapes = [((3, 9, 13, 16), (3, 3, 16, 32), (1, 1), (1, 1), "same", O.EXACT64),
+              ((2, 11, 10, 48), (3, 3, 48, 64), (2, 2), (1, 1), "same", O.WRAP32),
+              ((2, 12, 12, 64), (1, 1, 64, 96), (1, 1), (1, 1), "valid", O.SATURATE32),
+              ((1, 14, 9, 37), (3, 3, 37, 61), (1, 2), (2, 2), "same", O.EXACT64)]
+    for xs, fs, st, dil, pad, acc in shapes:
+        x = np.maximum(rng.standard_normal(xs), 0).astype(np.float32) if acc != O.WRAP32 else \
+            rng.uniform(-2, 3, xs).astype(np.float32)
+        case = dict(x=x, f=rng.standard_normal(fs).astype(np.float32), lut=O.random_lut(rng, mode), mode=mode,
+                    padding=pad, strides=st, dilations=dil, accumulator=acc, round_mode=O.HALF_EVEN)
+        case.update(in_range=(float(x.min()), float(x.max())),
+                    f_range=(float(case["f"].min()), float(case["f"].max())))
+        want, want_acc = oracle_conv(case, return_acc=True)
+        for v in cms:
+            y, acc_got, kern = gpu_conv(case, ft_variant=v)
+            assert kern.startswith("cm32"), kern
+            assert bits_equal(y, want), (kern, xs, fs)
+            assert np.array_equal(acc_got, want_acc), (kern, xs, fs)
