@@ -164,6 +164,8 @@ def kernel_family(variant_name: str) -> str:
     """Kernel behind a variant name reported by axb_last_kernel()."""
     if variant_name.startswith("ft"):
         return "lutconv_ft"
+    if variant_name.startswith("cm"):
+        return "lutconv_ftcm"
     if variant_name.startswith("lutconv_"):
         return variant_name
     if variant_name.startswith("depthwise"):

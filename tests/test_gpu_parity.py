@@ -838,3 +838,27 @@ def test_code_major_variants_vs_oracle(mode):
             assert kern.startswith("cm32"), kern
             assert bits_equal(y, want), (kern, xs, fs)
             assert np.array_equal(acc_got, want_acc), (kern, xs, fs)
+
+
+def test_graph_forced_code_major_matches_reference():
+    """Every ResNet-8 layer with 32-channel blocks forced onto each code-major variant (fused bias,
+    residual, ReLU, next-layer range in its epilogue; projections reading shared codes): logits
+    bit-identical to the reference executor's golden logits."""
+    torch = _torch()
+    from paper_2002_09481_b200 import _lib, resnet
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    lib = _lib.load()
+    g = load_golden("nets")
+    gg = GpuGraph(resnet.cifar_resnet(1, T.truncated_lut(T.Signedness.SIGNED, 2), seed=0))
+    x = torch.from_numpy(g["r8_trunc2_x"]).cuda()
+    gg.run(x)
+    for v in [v for v in range(1, lib.axb_ft_variant_count()) if lib.axb_ft_variant_layout(v) == 1]:
+        picks = {nid: (v if p.layer.ftable_cm is not None else 0) for nid, p in gg.conv_plans.items()}
+        assert sum(1 for p in picks.values() if p) >= 5, picks
+        gg.set_tuning(picks)
+        prof = []
+        y = gg.run(x, profile=prof).cpu().numpy()
+        assert sum(1 for *_, fam in prof if fam == "lutconv_ftcm") == sum(1 for p in picks.values() if p)
+        assert bits_equal(y, g["r8_trunc2_logits"]), lib.axb_ft_variant_name(v)
