@@ -1,38 +1,54 @@
 #!/usr/bin/env python
 """Benchmark: approximate-LUT ResNet inference on B200 (one process per GPU).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload r8|r50|r62] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload r50|r8|r62|r62sweep]
+                    [--impl b200|reference] [--stub]
 
 A step = one range-batch of synthetic images through the whole transformed
 ResNet graph (every conv an AxConv2D with the approximate truth table, the
 classifier a 1x1 AxConv2D): range reduction, quantize + zp-pad, LUT implicit
 GEMM with fused correction/dequant/bias/residual/ReLU/next-range epilogue,
-pools.  Default workload = BASELINE.json configs[1]: ResNet-8 CIFAR-10,
-batch 1024 per GPU, truncated_lut(signed, 2).
+pools.  Default workload = the north-star target, BASELINE configs[2]:
+ResNet-50 224x224, batch 256 per GPU, truncated_lut(signed, 2), calibrated
+weights (resnet.py).
 
-Data parallel by range-batch (ranges are per batch, graph.py:270-275): each
-rank runs its own batch with zero per-layer communication ("scaling": "weak");
-NCCL only all-gathers logits and all-reduces prediction counts after the
-timed region.  Timing: W warm-up steps, then K steps bracketed by barrier +
-synchronize; each step is timed with CUDA events on the launching stream and
-L2 is flushed (256 MiB write) between steps outside the events; the job
-time is the max over ranks.
+``--gpus N`` without a torch.distributed environment re-launches this script
+under ``python -m torch.distributed.run`` with N local ranks (127.0.0.1, NCCL,
+``NCCL_DEBUG=INFO`` limited to the INIT subsystem so every rank prints its
+communicator line).  Launched by torchrun directly, it uses the environment's
+ranks.  Sharding: range-batches (ranges are per batch,
+graph.py:270-275) -- every rank runs its own batch, zero per-layer
+communication ("scaling": "weak"); config 4 (``r62sweep``) -- the 32 candidate
+tables are dealt round-robin, uneven counts allowed ("scaling": "strong").
+NCCL only all-gathers logits and all-reduces prediction counts and device
+times after the timed region.
 
-value = approximate GMAC/s of the whole job (algorithmic MACs as
-graph_mac_count, graph.py:316-349); images/s alongside.  e2e = the same
-metric through the public GpuGraph.run API from pinned HOST batches, H2D copy
-of the images and D2H copy of the logits inside the timed region.
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize; each
+step is timed with CUDA events on the launching stream and L2 is flushed
+(256 MiB write) between steps outside the events; the job time is the max
+over ranks.  value = approximate GMAC/s of the whole job (algorithmic MACs as
+graph_mac_count, graph.py:316-349); images/s alongside.  e2e = the same metric
+through the public GpuGraph.run_pipelined API from pinned HOST batches, H2D
+of the inputs and D2H of the logits inside the timed region.  After the timed
+region rank 0's logits are compared bit-for-bit (sha256) with the real
+reference's output for the same batch (tests/golden/bench.npz): "parity".
 
---impl reference: the reference's CPU algorithm (the pinned oracle port:
-numpy + C/OpenMP LUT-GEMM, all host threads) on a bounded sample of the same
-workload, rank 0 only.
+--impl reference: the reference's CPU algorithm on the host cores (the pinned
+oracle port: numpy + C/OpenMP LUT-GEMM, all host threads; plus the real numba
+``axemu`` package from baseline/_ref when present) on bounded samples of the
+same workload, rank 0 only.
+
+--stub: the launcher / sharding / gather / JSON path on CPU with gloo and a
+synthetic step (no GPU) -- what the CPU tests exercise.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -48,6 +64,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "approximate GMAC/s and images/s (ResNet, synthetic) at 1/2/4/8 B200 vs CPU ref"
 # paper-derived GTX 1080 approximate throughput for the same CIFAR nets
 PAPER_GMACS = {"r8": 140.0, "r62": 95.5}
+BENCH_SEED = 1000  # rank r's range-batch is seeded BENCH_SEED + r (tests/golden/make_golden.py)
 
 
 def workload_spec(name: str, lut_kind: str):
@@ -65,18 +82,18 @@ def workload_spec(name: str, lut_kind: str):
         lut_desc = "random_lut(signed, seed 123)"
     if name == "r8":
         return dict(nodes=resnet.cifar_resnet(1, lut, seed=0), batch=1024, kind="cifar", lut=lut_desc,
-                    desc="ResNet-8 CIFAR-10 (He 6n+2, n=1; 9 convs + 1x1 AxConv2D classifier)")
+                    desc="ResNet-8 CIFAR-10 (He 6n+2, n=1; 9 convs + 1x1 AxConv2D classifier), calibrated")
     if name == "r62":
         return dict(nodes=resnet.cifar_resnet(10, lut, seed=0), batch=1000, kind="cifar", lut=lut_desc,
-                    desc="ResNet-62 CIFAR-10 (He 6n+2, n=10; 63 convs + 1x1 AxConv2D classifier)")
+                    desc="ResNet-62 CIFAR-10 (He 6n+2, n=10; 63 convs + 1x1 AxConv2D classifier), calibrated")
     if name == "r50":
         return dict(nodes=resnet.resnet50(lut, seed=0), batch=256, kind="imagenet", lut=lut_desc,
-                    desc="ResNet-50 v1.5 224x224 (53 convs + 1x1 AxConv2D classifier), BN folded")
+                    desc="ResNet-50 v1.5 224x224 (53 convs + 1x1 AxConv2D classifier), BN folded, calibrated")
     if name == "r62sweep":
         return dict(nodes=resnet.cifar_resnet(10, sweep_luts()[0], seed=0), batch=1000, kind="cifar",
                     lut="32 candidates: truncated_lut(mode, d) d=0..7 x {signed, unsigned} + 16 perturbed_lut "
                         "(exact + uniform error of 2..256, both signedness)",
-                    desc="ResNet-62 CIFAR-10 multiplier sweep over 32 candidate tables (config 4)",
+                    desc="ResNet-62 CIFAR-10 multiplier sweep over 32 candidate tables (config 4), calibrated",
                     sweep=True)
     raise SystemExit(f"unknown workload {name}")
 
@@ -99,17 +116,11 @@ def sweep_luts():
     return luts
 
 
-def build_graphs(spec, name, world, rank, device):
-    """This rank's networks: one graph, or its shard of the candidate tables (config 4)."""
-    from paper_2002_09481_b200 import resnet
+def units_of(spec, world: int, rank: int) -> list[int]:
+    """This rank's networks: [0] (its own range-batch) or its round-robin share of the 32 tables."""
     from paper_2002_09481_b200.dist import shard
-    from paper_2002_09481_b200.graph import GpuGraph
 
-    if not spec.get("sweep"):
-        return [GpuGraph(spec["nodes"], device=device)], [0]
-    luts = sweep_luts()
-    mine = shard(len(luts), world, rank)
-    return [GpuGraph(resnet.cifar_resnet(10, luts[i], seed=0), device=device) for i in mine], mine
+    return shard(len(sweep_luts()), world, rank) if spec.get("sweep") else [0]
 
 
 def make_images(kind: str, n: int, seed: int):
@@ -117,14 +128,55 @@ def make_images(kind: str, n: int, seed: int):
 
     if kind == "cifar":
         return datasets.synthetic_cifar10(n, seed=seed)
-    return datasets.uniform_images(n, 224, seed=seed), np.zeros(n, np.uint8)
+    return datasets.synthetic_imagenet(n, seed=seed)
+
+
+def make_config(spec, args, batch: int, world: int, macs_img: int) -> dict:
+    """The workload description shared by both arms (same dict -> same config)."""
+    return {"workload": spec["desc"], "batch_per_gpu": batch, "lut": spec["lut"],
+            "networks": 32 if spec.get("sweep") else 1, "macs_per_image": macs_img,
+            "images": f"synthetic_{'cifar10' if spec['kind'] == 'cifar' else 'imagenet'}(batch, seed="
+                      f"{BENCH_SEED} + rank)" if not spec.get("sweep") else
+                      f"synthetic_cifar10(batch, seed={BENCH_SEED}), every candidate table",
+            "parallelism": (f"dp{world} (candidate tables sharded round-robin)" if spec.get("sweep")
+                            else f"dp{world} (one range-batch per GPU)"),
+            "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+
+
+# ---------------------------------------------------------------------------- launcher
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args, argv) -> int:
+    """Re-run this script under torch.distributed.run with ``args.gpus`` local ranks."""
+    if not args.stub:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {have} visible CUDA "
+                                                         "devices"}), flush=True)
+            return 1
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "4")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()), *argv]
+    print("[bench] launching:", " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 # ---------------------------------------------------------------------------- clocks
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons, sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 20 ms during the timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -182,7 +234,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---------------------------------------------------------------------------- CPU baseline
+# ---------------------------------------------------------------------------- CPU baselines
 
 
 def oracle_nodes(nodes):
@@ -195,14 +247,15 @@ def oracle_nodes(nodes):
     return out
 
 
-def cpu_reference_rate(spec, macs_per_img: int, budget_s: float, seed: int = 0):
+def cpu_reference_rate(spec, macs_per_img: int, budget_s: float, seed: int = 0, warm: bool = True):
     """Time the oracle port (reference algorithm, all host threads) on a bounded sample."""
     from oracle import axemu_oracle as O
 
     onodes = oracle_nodes(spec["nodes"])
     n = 2 if spec["kind"] == "imagenet" else 16
     x, _ = make_images(spec["kind"], n, seed)
-    O.run_graph(onodes, x[:1])  # warm-up (page-in, OpenMP pool)
+    if warm:
+        O.run_graph(onodes, x[:1])  # warm-up (page-in, OpenMP pool)
     t0 = time.perf_counter()
     O.run_graph(onodes, x)
     dt = time.perf_counter() - t0
@@ -217,102 +270,174 @@ def cpu_reference_rate(spec, macs_per_img: int, budget_s: float, seed: int = 0):
         n = n2
     gmacs = n * macs_per_img / dt / 1e9
     return dict(value=round(gmacs, 4), unit="GMAC/s", images_per_s=round(n / dt, 3), cores=O.threads(),
-                kind="port", sample=f"{n} images of the same workload through the oracle port "
-                                    f"(numpy + C/OpenMP int64 LUT-GEMM), {dt:.2f} s")
+                kind="port", images=n, seconds=round(dt, 3),
+                sample=f"{n} images of the same workload through the oracle port "
+                       f"(numpy + C/OpenMP int64 LUT-GEMM), {dt:.2f} s")
 
 
-# ---------------------------------------------------------------------------- main
+def reference_numba_rate(spec, macs_per_img: int, budget_s: float, seed: int = 0):
+    """The real reference package (axemu, numba ``gemm`` engine, all host threads) from baseline/_ref,
+    if it was installed there; None otherwise."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "axemu").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/axemu_numba_cache")
+    sys.path.insert(0, str(ref))
+    try:
+        import numba
+        import axemu
+        from axemu import LayerGraph, Layout, MultLut, Node, NodeKind, Signedness, Tensor4
+    except Exception as e:  # pragma: no cover - depends on the box
+        return {"unavailable": f"import failed: {e}"}
+    ref_nodes = []
+    for nd in spec["nodes"]:
+        a = dict(nd["attrs"])
+        if "lut" in a:
+            a["lut"] = MultLut(Signedness(a["lut"].mode.value), a["lut"].entries)
+        ref_nodes.append(Node(nd["id"], NodeKind(nd["kind"]), list(nd["inputs"]), a))
+    g = LayerGraph(ref_nodes)
+    n = 2 if spec["kind"] == "imagenet" else 16
+    x, _ = make_images(spec["kind"], n, seed)
+    t0 = time.perf_counter()
+    axemu.run(g, Tensor4(x[:1], Layout.NHWC), "gemm")  # warm-up: numba JIT (cached under NUMBA_CACHE_DIR)
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    axemu.run(g, Tensor4(x, Layout.NHWC), "gemm")
+    dt = time.perf_counter() - t0
+    scale = max(1, min(int(budget_s / max(dt, 1e-3)), 64 if spec["kind"] == "cifar" else 4))
+    if scale > 1:
+        n *= scale
+        x, _ = make_images(spec["kind"], n, seed)
+        t0 = time.perf_counter()
+        axemu.run(g, Tensor4(x, Layout.NHWC), "gemm")
+        dt = time.perf_counter() - t0
+    return dict(value=round(n * macs_per_img / dt / 1e9, 4), unit="GMAC/s", images_per_s=round(n / dt, 3),
+                cores=int(numba.config.NUMBA_NUM_THREADS), kind="reference", t_init_s=round(t_init, 2),
+                sample=f"{n} images through the real axemu.graph.run(engine='gemm') (numba, baseline/_ref), "
+                       f"{dt:.2f} s after a 1-image warm-up")
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="r8", choices=["r8", "r50", "r62", "r62sweep"])
-    ap.add_argument("--lut", default="trunc2", choices=["trunc2", "exact", "random"])
-    ap.add_argument("--batch", type=int, default=0)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--layers-out", default="")
-    ap.add_argument("--no-autotune", action="store_true", help="use the cost model's kernel variants")
-    ap.add_argument("--tuned-out", default="", help="write the autotuned per-layer variants (json)")
-    ap.add_argument("--tuned-from", default="", help="use per-layer variants from a --tuned-out file")
-    ap.add_argument("--report-out", default="",
-                    help="also write a RunReport (t_init + t_comp, phase split; reference bench.py:37-87) of "
-                         "benchmark.run_benchmark over --steps batches: <path>.json and <path>.csv")
-    args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    spec = workload_spec(args.workload, args.lut)
-    batch = args.batch or spec["batch"]
-    from paper_2002_09481_b200 import resnet
-
-    macs_img = resnet.macs_per_image(spec["nodes"])
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        steps = []
-        for _ in range(args.warmup):
-            pass
-        info = None
-        for k in range(max(1, args.steps)):
-            info = cpu_reference_rate(spec, macs_img, budget_s=min(args.cpu_budget, 20.0), seed=k)
-            steps.append(info["value"])
-        val = statistics.median(steps)
-        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GMAC/s",
-                "images_per_s": round(val * 1e9 / macs_img, 3), "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "higher_is_better": True,
-                "scaling": "strong" if spec.get("sweep") else "weak", "vs_baseline": None,
-                "dtype": "u8", "data": "synthetic",
-                "config": {"workload": spec["desc"], "batch_per_gpu": batch, "lut": spec["lut"]},
-                "cpu_baseline": {"value": val, "unit": "GMAC/s", "cores": info["cores"], "kind": "port",
-                                 "sample": info["sample"]},
-                "e2e": {"value": val, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+def reference_arm(args, spec, batch, world, rank, macs_img):
+    """--impl reference: the reference's CPU implementation on the host cores, rank 0 only."""
+    if rank != 0:
         return
+    from oracle import axemu_oracle as O
 
+    onodes = oracle_nodes(spec["nodes"])
+    xw, _ = make_images(spec["kind"], 1, 999)
+    for _ in range(args.warmup):  # W real warm-up passes (page-in, OpenMP pool) on a 1-image sample
+        O.run_graph(onodes, xw)
+    imgs = secs = 0.0
+    info = None
+    for k in range(max(1, args.steps)):
+        info = cpu_reference_rate(spec, macs_img, budget_s=min(args.cpu_budget, 20.0) / max(1, args.steps) * 2,
+                                  seed=k, warm=False)
+        imgs += info["images"]
+        secs += info["seconds"]
+    val = round(imgs * macs_img / secs / 1e9, 4)
+    numba_rate = None if args.no_numba else reference_numba_rate(spec, macs_img, budget_s=min(args.cpu_budget, 10))
+    cpu = {"value": val, "unit": "GMAC/s", "cores": info["cores"], "kind": "port",
+           "sample": f"{int(imgs)} images in {args.steps} steps of the same workload through the oracle port "
+                     f"(numpy + C/OpenMP int64 LUT-GEMM), {secs:.2f} s"}
+    if numba_rate is not None:
+        cpu["reference_numba"] = numba_rate
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GMAC/s",
+            "images_per_s": round(imgs / secs, 3), "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(secs * 1e3 / max(1, args.steps), 3), "higher_is_better": True,
+            "scaling": "strong" if spec.get("sweep") else "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic",
+            "config": make_config(spec, args, batch, world, macs_img),
+            "cpu_baseline": cpu,
+            "e2e": {"value": val, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- one rank's work
+
+
+class CpuEvent:
+    """torch.cuda.Event stand-in for --stub (host clock)."""
+
+    def __init__(self, enable_timing=True):
+        self.t = None
+
+    def record(self, stream=None):
+        self.t = time.perf_counter()
+
+    def elapsed_time(self, other) -> float:
+        return (other.t - self.t) * 1e3
+
+
+def stub_rank(args, spec, batch, ctx, units) -> dict:
+    """Synthetic step on the host: deterministic logits per (table, image), ~2 ms per network."""
+    classes = 10 if spec["kind"] == "cifar" else 1000
+    rng_seed = BENCH_SEED if spec.get("sweep") else BENCH_SEED + ctx["rank"]
+
+    def step():
+        ys = []
+        for u in units:
+            r = np.random.default_rng([rng_seed, u])
+            ys.append(r.standard_normal((batch, classes)).astype(np.float32))
+            time.sleep(0.002)
+        return np.stack(ys) if ys else np.zeros((0, batch, classes), np.float32)
+
+    for _ in range(args.warmup):
+        step()
+    ctx["barrier"]()
+    evs = []
+    for _ in range(args.steps):
+        e0, e1 = CpuEvent(), CpuEvent()
+        e0.record()
+        y = step()
+        e1.record()
+        evs.append((e0, e1))
+    ctx["barrier"]()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    _, labels = make_images(spec["kind"], batch, rng_seed) if spec["kind"] == "cifar" else (None, np.zeros(batch))
+    return {"total_ms": total_ms, "e2e_ms": total_ms, "conv_ms": 0.0, "logits": y, "labels": labels,
+            "launches": 0, "extra": {}}
+
+
+def device_rank(args, spec, batch, ctx, units) -> dict:
     import torch
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200.graph import GpuGraph
 
-        dist.init_process_group("nccl", device_id=dev)
-    graphs, lut_ids = build_graphs(spec, args.workload, world, rank, local)
-    nets = len(graphs)
-
-    def run_all(x, check=False, profile=None):
-        ys = [g.run(x, check=check, profile=profile) for g in graphs]
-        return ys
-
-    imgs, labels = make_images(spec["kind"], batch, seed=(1000 + rank) if not spec.get("sweep") else 1000)
+    dev = ctx["device"]
+    local = dev.index
+    if spec.get("sweep"):
+        luts = sweep_luts()
+        graphs = [GpuGraph(resnet.cifar_resnet(10, luts[i], seed=0), device=local) for i in units]
+    else:
+        graphs = [GpuGraph(spec["nodes"], device=local)]
+    seed = BENCH_SEED if spec.get("sweep") else BENCH_SEED + ctx["rank"]
+    imgs, labels = make_images(spec["kind"], batch, seed=seed)
     x_dev = torch.from_numpy(imgs).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    barrier = ctx["barrier"]
+
+    def run_all(x, check=False, profile=None, mprofile=None):
+        return [g.run(x, check=check, profile=profile, mprofile=mprofile) for g in graphs]
 
     # warm-up (also prepares filters once: hoisted quantize_filters), per-layer kernel autotune on the
     # first batch (outside the timed region; bit-identity of all variants checked), CUDA-graph capture
     for _ in range(args.warmup):
-        ys = run_all(x_dev, check=True)
-    if args.tuned_from:  # replay an earlier run's picks (e.g. under ncu, whose replays distort timing)
-        graphs[0].set_tuning(json.loads(Path(args.tuned_from).read_text()))
-        tuned = {"from": args.tuned_from}
-    else:
-        tuned = {} if args.no_autotune else graphs[0].autotune(x_dev)
-        if tuned and args.tuned_out:
-            Path(args.tuned_out).write_text(json.dumps(graphs[0].tuning()))
-    for g in graphs[1:]:  # same architecture (sweep candidates): same shapes -> same picks
-        if tuned:
-            g.copy_tuning(graphs[0])
+        run_all(x_dev, check=True)
+    tuned = {}
+    if graphs:
+        if args.tuned_from:  # replay an earlier run's picks (e.g. under ncu, whose replays distort timing)
+            graphs[0].set_tuning(json.loads(Path(args.tuned_from).read_text()))
+            tuned = {"from": args.tuned_from}
+        elif not args.no_autotune:
+            tuned = graphs[0].autotune(x_dev)
+            if args.tuned_out:
+                Path(args.tuned_out).write_text(json.dumps(graphs[0].tuning()))
+        for g in graphs[1:]:  # same architecture (sweep candidates): same shapes -> same picks
+            if tuned:
+                g.copy_tuning(graphs[0])
     torch.cuda.synchronize()
+    run_all(x_dev)
     launches = sum(g.launches for g in graphs)
     for g in graphs:
         g.capture(tuple(x_dev.shape))
@@ -320,55 +445,40 @@ def main():
         ys = [g.replay(x_dev) for g in graphs]
     torch.cuda.synchronize()
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
     # ------------------------------------------------ device-resident timed region (graph replay)
     sampler = ClockSampler(local)
     sampler.start()
     barrier()
-    step_ms = []
+    step_ev = []
     for _ in range(args.steps):
         flush.zero_()  # write > L2 (126 MB) between timed steps
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         ys = [g.replay(x_dev, check=False) for g in graphs]
         e1.record()
-        step_ms.append((e0, e1))
+        step_ev.append((e0, e1))
     barrier()
     clocks = sampler.stop()
-    per_step = [a.elapsed_time(b) for a, b in step_ms]
-    total_ms = sum(per_step)
+    total_ms = sum(a.elapsed_time(b) for a, b in step_ev)
     for g in graphs:
         g.check_flags()
-    y = torch.stack([t.reshape(batch, -1) for t in ys])  # (nets, batch, classes)
+    y = torch.stack([t.reshape(batch, -1) for t in ys]) if ys else torch.zeros((0, batch, 1), device=dev)
 
-    # ------------------------------------------------ LUT-conv kernel times (eager pass, events per launch)
+    # ------------------------------------------------ per-kernel times (eager pass, events per launch)
     profile: list = []
+    mprofile: list = []
     barrier()
     for _ in range(args.steps):
         flush.zero_()
-        run_all(x_dev, profile=profile)
+        run_all(x_dev, profile=profile, mprofile=mprofile)
     barrier()
-    conv_ms = sum(a.elapsed_time(b) for _, a, b, _, _, _ in profile) / args.steps
-    conv_macs = sum(m for _, _, _, m, _, _ in profile) / args.steps
-    conv_algo_bytes = sum(ab for *_, ab, _ in profile) / args.steps
-    conv_launches = len(profile) // args.steps
-    layer_rows = {}
-    for nid, a, b, m, _, _ in profile:
-        r = layer_rows.setdefault(nid, [0.0, 0, 0])
-        r[0] += a.elapsed_time(b)
-        r[1] += m
-        r[2] += 1
+    torch.cuda.synchronize()
 
     # ------------------------------------------------ end-to-end through the public API (host buffers)
-    # GpuGraph.run_pipelined: pinned host batch -> H2D (copy stream, overlapping the previous
-    # step's compute) -> captured step -> D2H of the logits (+ flags); L2 flushed before each step.
-    # CIFAR workloads: the host batch is the CIFAR-10 binary record array (the reference's on-disk
-    # input, formats.py:131-171), decoded on the device inside the captured step; ImageNet-shaped
-    # workloads ship fp32 NHWC images.
+    # GpuGraph.run_pipelined: pinned host batch -> H2D (copy stream, overlapping the previous step's
+    # compute) -> captured step -> D2H of the logits (+ flags); L2 flushed before each step.  CIFAR
+    # workloads ship the CIFAR-10 binary records (the reference's on-disk input, formats.py:131-171),
+    # decoded on the device inside the captured step; ImageNet-shaped workloads ship fp32 NHWC images.
     if spec["kind"] == "cifar":
         from paper_2002_09481_b200.formats import encode_cifar10
 
@@ -389,11 +499,11 @@ def main():
         g.run_pipelined(x_hosts, o, before_step=flush.zero_)
     e1.record()
     barrier()
-    e2e_total = e0.elapsed_time(e1)
+    e2e_ms = e0.elapsed_time(e1)
     for o, t in zip(outs, ys):  # the host logits of the last e2e step == the device-timed run's
         assert torch.equal(o[-1].view(torch.int32), t.cpu().view(torch.int32))
 
-    if args.report_out and rank == 0:  # the reference harness's report, from the GPU engine (outside the region)
+    if args.report_out and ctx["rank"] == 0 and graphs:  # the reference harness's report (outside the region)
         from paper_2002_09481_b200.benchmark import run_benchmark
         from paper_2002_09481_b200.formats import report_csv, save_report
 
@@ -402,91 +512,234 @@ def main():
         save_report(report, args.report_out + ".json")
         Path(args.report_out + ".csv").write_text(report_csv(report))
 
-    # ------------------------------------------------ max over ranks, NCCL gather of logits/counts
-    from paper_2002_09481_b200.dist import exchange_results
+    conv_ms = sum(a.elapsed_time(b) for _, a, b, _, _, _ in profile) / args.steps
+    extra = {"profile": profile, "mprofile": mprofile, "clocks": clocks, "tuned": tuned, "graphs": graphs,
+             "h2d": int(x_hosts[0].numel() * x_hosts[0].element_size() * len(graphs)),
+             "d2h": int(sum(o[0].numel() * 4 + g.flags.numel() * 4 for g, o in zip(graphs, outs))),
+             "e2e_path": "GpuGraph.run_pipelined: pinned host batch ("
+                         + ("CIFAR-10 binary records, decoded on the device" if spec["kind"] == "cifar"
+                            else "fp32 NHWC images")
+                         + "), H2D on a copy stream overlapping the previous step, CUDA-graph step, D2H of "
+                           "logits + flags; L2 flushed before every step inside the region"}
+    return {"total_ms": total_ms, "e2e_ms": e2e_ms, "conv_ms": conv_ms, "logits": y, "labels": labels,
+            "launches": launches, "extra": extra}
 
-    t = torch.tensor([total_ms, e2e_total, conv_ms], dtype=torch.float64, device=dev)
-    logits = y  # (nets, batch, classes)
-    pred = logits.argmax(-1)
-    agree = (pred.cpu().numpy() == labels.astype(np.int64)[None, :]).sum(1)  # per network
-    cnt = torch.tensor(list(agree) + [batch * nets], dtype=torch.int64, device=dev)
-    gathered, cnt, t = exchange_results(logits, cnt, t)
-    total_ms, e2e_total, conv_ms_max = (float(v) for v in t.tolist())
-    if rank != 0:
-        dist.destroy_process_group()
-        return
 
-    images = batch * nets * world * args.steps  # image x network evaluations
-    gmacs = images * macs_img / (total_ms / 1e3) / 1e9
-    e2e_gmacs = images * macs_img / (e2e_total / 1e3) / 1e9
+# ---------------------------------------------------------------------------- roofline / HBM blocks
 
-    import json as _json
 
-    peaks = {}
-    try:
-        peaks = _json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except Exception:
-        pass
-    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-    max_mhz = float(peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0)
-    # Shared-memory lookup roofline of the product gather: 128 B per SM per clock (one wavefront of
-    # 32 four-byte banks) / 2 B per 16-bit product = 64 lookups/clk/SM.  The ftable kernel reaches it
-    # with two products per bank word; the north_star's LDS.16 roofline (one lookup per lane per
-    # wavefront, 32/clk/SM) is reported alongside.
-    theo_lookups = sm_count * 64 * max_mhz * 1e6
-    lds16_lookups = sm_count * 32 * max_mhz * 1e6
-    # measured shared-memory gather roofline (scripts/smem_roofline.cu): conflict-free warp gathers
-    # of 64/128-bit words = the bandwidth bound as this B200 delivers it; LDS.32 with the kernel's
-    # packed-pair accumulation mix alongside
+def roofline_block(args, res, sm_count, max_mhz, sampled, total_ms):
+    prof = res["extra"]["profile"]
+    steps = args.steps
+    conv_ms = sum(a.elapsed_time(b) for _, a, b, _, _, _ in prof) / steps
+    conv_macs = sum(m for _, _, _, m, _, _ in prof) / steps
+    conv_algo_bytes = sum(ab for *_, ab, _ in prof) / steps
+    launches = len(prof) // steps
+    theo = sm_count * 64 * max_mhz * 1e6
+    lds16 = sm_count * 32 * max_mhz * 1e6
     measured = {}
     try:
-        measured = _json.loads((ROOT / "profiles" / "smem_roofline.json").read_text())["products_per_s"]
+        measured = json.loads((ROOT / "profiles" / "smem_roofline.json").read_text())["products_per_s"]
     except Exception:
         measured = {}
-    peak_lookups = max(measured.get("lds64", 0.0), measured.get("lds128", 0.0)) or theo_lookups
+    peak = max(measured.get("lds64", 0.0), measured.get("lds128", 0.0)) or theo
     achieved = conv_macs / (conv_ms / 1e3) if conv_ms else 0.0
-    sampled = clocks.get("sm_mhz")
+    # per kernel family: launches, average launch, share of the step
+    fam: dict = {}
+    for _, a, b, m, _, k in prof:
+        r = fam.setdefault(k, [0, 0.0, 0])
+        r[0] += 1
+        r[1] += a.elapsed_time(b)
+        r[2] += m
+    step_ms = total_ms / steps
+    kernels = {k: {"launches_per_step": v[0] // steps, "avg_us": round(v[1] / v[0] * 1e3, 2),
+                   "share_of_step": round(v[1] / steps / step_ms, 4),
+                   "glookup_s": round(v[2] / (v[1] / 1e3) / 1e9, 1)} for k, v in fam.items()}
+    dominant = max(kernels, key=lambda k: kernels[k]["share_of_step"]) if kernels else None
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.workload}.json"
     if tf.exists():
         try:
-            traffic = _json.loads(tf.read_text()).get("dram_bytes_per_launch")
+            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    kernels = sorted({k for *_, k in profile})
-    # measured bank-conflict share of the kernel's shared-memory wavefronts (committed ncu capture):
-    # with the LDS pipe 100% busy the kernel could reach at most (1 - conflict) of `peak`
     conflict = None
     cf = ROOT / "profiles" / "conflicts.json"
     if cf.exists():
         try:
-            captured = _json.loads(cf.read_text()).get("r8" if args.workload == "r8" else "r50", [])
+            captured = json.loads(cf.read_text()).get(args.workload, [])
             if captured:
                 conflict = sum(x["bank_conflict_wavefronts"] for x in captured) / sum(
                     x["shared_ld_wavefronts"] for x in captured)
         except Exception:
             conflict = None
-    roofline = {
-        "bound": "smem", "kernel": "LUT-product gather conv, all conv launches of a step: " + ", ".join(kernels),
-        "achieved": round(achieved / 1e9, 2), "peak": round(peak_lookups / 1e9, 2), "unit": "Glookup/s",
-        "frac": round(achieved / peak_lookups, 4),
-        "frac_at_sampled_clock": round(achieved / peak_lookups * max_mhz / sampled, 4) if sampled else None,
+    return {
+        "bound": "smem", "kernel": "LUT-product gather conv, all conv launches of a step",
+        "dominant_kernel": dominant, "kernels": kernels,
+        "achieved": round(achieved / 1e9, 2), "peak": round(peak / 1e9, 2), "unit": "Glookup/s",
+        "frac": round(achieved / peak, 4),
+        "frac_at_sampled_clock": round(achieved / peak * max_mhz / sampled, 4) if sampled else None,
         "peak_basis": ("measured: conflict-free LDS.64/LDS.128 warp gathers of 16-bit products "
                        "(profiles/smem_roofline.json, scripts/smem_roofline.cu)") if measured else
                       (f"derived: {sm_count} SMs x 128 B/clk / 2 B per product x {max_mhz:.0f} MHz"),
-        "peak_theoretical": round(theo_lookups / 1e9, 2),
+        "peak_theoretical": round(theo / 1e9, 2),
         "peak_lds32_gather_measured": round(measured["lds32"] / 1e9, 2) if measured else None,
-        "frac_of_lds32_gather_peak": round(achieved / measured["lds32"], 4) if measured else None,
         "lds_conflict_wavefront_frac": round(conflict, 4) if conflict is not None else None,
-        "frac_of_conflict_bound": round(achieved / theo_lookups / (1 - conflict), 4) if conflict else None,
         "conflict_basis": "profiles/conflicts.json (ncu l1tex shared-load bank conflicts / wavefronts)",
-        "lds16_lookup_roofline": round(lds16_lookups / 1e9, 2),
-        "frac_vs_lds16_lookup_roofline": round(achieved / lds16_lookups, 4),
+        "lds16_lookup_roofline": round(lds16 / 1e9, 2),
+        "frac_vs_lds16_lookup_roofline": round(achieved / lds16, 4),
         "traffic": traffic, "traffic_unit": "DRAM bytes per LUT-conv launch (ncu --set full, committed profile)",
-        "algorithmic_bytes_per_launch": int(conv_algo_bytes / max(conv_launches, 1)),
-        "conv_launches_per_step": conv_launches,
-        "conv_share_of_step": round(conv_ms / (total_ms / args.steps), 4) if total_ms else None,
+        "algorithmic_bytes_per_launch": int(conv_algo_bytes / max(launches, 1)),
+        "conv_launches_per_step": launches,
+        "conv_share_of_step": round(conv_ms / step_ms, 4) if total_ms else None,
     }
+
+
+def hbm_block(args, res, peak_gbs):
+    """GB/s of the memory-bound kernels (range, record decode, quantize, pools, add) from the eager
+    pass: algorithmic bytes (4 B per fp32 element read / written, 1 B per code) / event-timed launch."""
+    agg: dict = {}
+    for _, kind, a, b, nbytes in res["extra"]["mprofile"]:
+        r = agg.setdefault(kind, [0, 0.0, 0])
+        r[0] += 1
+        r[1] += a.elapsed_time(b)
+        r[2] += nbytes
+    out = {"peak_gbs": peak_gbs, "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy test)", "kernels": {}}
+    tb = tm = 0.0
+    for k, (n, ms, nb) in sorted(agg.items()):
+        gbs = nb / (ms / 1e3) / 1e9 if ms else 0.0
+        out["kernels"][k] = {"launches_per_step": n // args.steps, "ms_per_step": round(ms / args.steps, 4),
+                             "bytes_per_step": int(nb / args.steps), "gbs": round(gbs, 1),
+                             "frac": round(gbs / peak_gbs, 4) if peak_gbs else None}
+        tb += nb
+        tm += ms
+    out["all"] = {"gbs": round(tb / (tm / 1e3) / 1e9, 1) if tm else None,
+                  "frac": round(tb / (tm / 1e3) / 1e9 / peak_gbs, 4) if tm and peak_gbs else None,
+                  "share_of_step": round(tm / res["total_ms"], 4) if res["total_ms"] else None}
+    return out
+
+
+def parity_block(args, spec, batch, y_rank0) -> dict:
+    """Rank 0's logits vs the real reference's for the same batch (tests/golden/bench.npz)."""
+    path = ROOT / "tests" / "golden" / "bench.npz"
+    key = f"{args.workload}_logits_sha"
+    if spec.get("sweep") or batch != spec["batch"] or args.lut != "trunc2" or not path.exists():
+        return {"status": "unchecked", "why": "no reference golden for this workload / batch / table"}
+    g = np.load(path)
+    if key not in g:
+        return {"status": "unchecked", "why": f"{key} missing from tests/golden/bench.npz"}
+    got = np.ascontiguousarray(y_rank0.reshape(batch, 1, 1, -1).astype(np.float32))
+    sha = hashlib.sha256(got.tobytes()).digest()
+    am = got.reshape(batch, -1).argmax(1)
+    ok = sha == g[key].tobytes() and np.array_equal(am, g[f"{args.workload}_argmax"])
+    return {"status": "bit-exact" if ok else "MISMATCH",
+            "against": f"tests/golden/bench.npz {key}: sha256 of all {batch} logits rows from the real reference "
+                       "graph.run (engine gemm) on the same batch, weights and table",
+            "logits_sha256": sha.hex(), "argmax_distinct_classes": int(len(set(am.tolist())))}
+
+
+# ---------------------------------------------------------------------------- main
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="r50", choices=["r8", "r50", "r62", "r62sweep"])
+    ap.add_argument("--lut", default="trunc2", choices=["trunc2", "exact", "random"])
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--stub", action="store_true", help="CPU/gloo synthetic step: launcher + sharding + JSON only")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-numba", action="store_true", help="skip the real-reference (numba) CPU timing")
+    ap.add_argument("--layers-out", default="")
+    ap.add_argument("--no-autotune", action="store_true", help="use the cost model's kernel variants")
+    ap.add_argument("--tuned-out", default="", help="write the autotuned per-layer variants (json)")
+    ap.add_argument("--tuned-from", default="", help="use per-layer variants from a --tuned-out file")
+    ap.add_argument("--report-out", default="",
+                    help="also write a RunReport (t_init + t_comp, phase split; reference bench.py:37-87) of "
+                         "benchmark.run_benchmark over --steps batches: <path>.json and <path>.csv")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":  # the CPU arm runs once, on "rank 0"
+            os.environ.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+        else:
+            sys.exit(launch_ranks(args, argv))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    spec = workload_spec(args.workload, args.lut)
+    batch = args.batch or spec["batch"]
+    from paper_2002_09481_b200 import resnet
+
+    macs_img = resnet.macs_per_image(spec["nodes"])
+    if args.impl == "reference":
+        return reference_arm(args, spec, batch, world, rank, macs_img)
+
+    import torch
+
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dist = None
+    if args.stub:
+        dev = torch.device("cpu")
+    else:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        if args.stub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        if not args.stub:
+            torch.cuda.synchronize()
+
+    ctx = {"rank": rank, "world": world, "device": dev, "barrier": barrier}
+    units = units_of(spec, world, rank)
+    res = (stub_rank if args.stub else device_rank)(args, spec, batch, ctx, units)
+
+    # ------------------------------------------------ max over ranks, NCCL gather of logits/counts
+    from paper_2002_09481_b200.dist import exchange_results
+
+    logits = res["logits"] if isinstance(res["logits"], torch.Tensor) else torch.from_numpy(res["logits"])
+    logits = logits.to(dev)
+    labels = np.asarray(res["labels"]).astype(np.int64)
+    pred = logits.argmax(-1).cpu().numpy() if logits.numel() else np.zeros((0, batch), np.int64)
+    agree = (pred == labels[None, :]).sum(1) if len(pred) else np.zeros(0, np.int64)
+    cnt = torch.tensor([int(agree.sum()), batch * len(units)], dtype=torch.int64, device=dev)
+    t = torch.tensor([res["total_ms"], res["e2e_ms"], res["conv_ms"]], dtype=torch.float64, device=dev)
+    gathered, cnt, t = exchange_results(logits, cnt, t)
+    unit_lists = [units]
+    if dist is not None:
+        unit_lists = [None] * world
+        dist.all_gather_object(unit_lists, units)
+    total_ms, e2e_ms, _ = (float(v) for v in t.tolist())
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    nets_total = sum(len(u) for u in unit_lists)
+    images = batch * nets_total * args.steps  # image x network evaluations over all ranks
+    gmacs = images * macs_img / (total_ms / 1e3) / 1e9
+    e2e_gmacs = images * macs_img / (e2e_ms / 1e3) / 1e9
+    flat = sorted(i for u in unit_lists for i in u)
+    units_info = {"kind": "candidate tables" if spec.get("sweep") else "range-batches",
+                  "per_rank": [len(u) for u in unit_lists], "total": nets_total,
+                  "covered_once": flat == list(range(32 if spec.get("sweep") else 1)) if spec.get("sweep")
+                  else nets_total == world}
     line = {
         "metric": METRIC, "value": round(gmacs, 2), "unit": "GMAC/s",
         "images_per_s": round(images / (total_ms / 1e3), 2), "n_gpus": world, "steps": args.steps,
@@ -494,39 +747,71 @@ def main():
         # range-batches: fixed batch per GPU (weak); the 32-table sweep: fixed job split over ranks (strong)
         "scaling": "strong" if spec.get("sweep") else "weak",
         "vs_baseline": round(gmacs / PAPER_GMACS[args.workload], 2) if args.workload in PAPER_GMACS else None,
-        "vs_baseline_basis": "paper-derived GTX 1080 approx GMAC/s (BASELINE.md s1)" if args.workload in PAPER_GMACS else None,
+        "vs_baseline_basis": ("paper-derived GTX 1080 approx GMAC/s (BASELINE.md s1)"
+                              if args.workload in PAPER_GMACS else "no published number for this config"),
         "dtype": "u8", "data": "synthetic",
-        "config": {"workload": spec["desc"], "batch_per_gpu": batch, "lut": spec["lut"],
-                   "networks_per_gpu": nets, "macs_per_image": macs_img,
-                   "parallelism": (f"dp{world} (candidate tables sharded round-robin)" if spec.get("sweep")
-                                   else f"dp{world} (one range-batch per GPU)"),
-                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "step": "one CUDA-graph replay of the whole graph (captured after warm-up)",
-                   "kernel_variants": "autotuned per layer on the first batch" if tuned else "cost model"},
-        "roofline": roofline,
-        "e2e": {"value": round(e2e_gmacs, 2), "unit": "GMAC/s", "images_per_s": round(images / (e2e_total / 1e3), 2),
-                "h2d_bytes_per_step": int(x_hosts[0].numel() * x_hosts[0].element_size() * nets),
-                "d2h_bytes_per_step": int(sum(o[0].numel() * 4 + g.flags.numel() * 4 for g, o in zip(graphs, outs))),
-                "path": "GpuGraph.run_pipelined: pinned host batch ("
-                        + ("CIFAR-10 binary records, decoded on the device" if spec["kind"] == "cifar"
-                           else "fp32 NHWC images")
-                        + "), H2D on a copy stream overlapping the previous step, CUDA-graph step, D2H of "
-                          "logits + flags; L2 flushed before every step inside the region"},
-        "gpu_launches": launches * args.steps,
-        "clocks": clocks,
-        "agreement_with_labels": round(float(cnt[:-1].sum()) / float(cnt[-1]), 4),
+        "config": make_config(spec, args, batch, world, macs_img),
+        "units": units_info,
+        "agreement_with_labels": round(float(cnt[0]) / float(cnt[1]), 4) if float(cnt[1]) else None,
     }
+    if args.stub:
+        line["stub"] = "synthetic host step (no GPU): launcher, sharding, gather and JSON path only"
+        line["logits_gathered"] = list(gathered.shape) if hasattr(gathered, "shape") else [len(gathered)]
+        print(json.dumps(line), flush=True)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    ex = res["extra"]
+    clocks = ex["clocks"]
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    max_mhz = float(peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0)
+    y0 = res["logits"][0].cpu().numpy() if len(units) else None
+    line["parity"] = parity_block(args, spec, batch, y0) if y0 is not None else {"status": "unchecked"}
+    # rank 0's device time alone feeds the per-kernel blocks (same GPU model on every rank)
+    line["roofline"] = roofline_block(args, res, sm_count, max_mhz, clocks.get("sm_mhz"), res["total_ms"])
+    hbm_peak = float(peaks.get("hbm_gbs") or 6550.0)
+    line["hbm"] = hbm_block(args, res, hbm_peak)
+    line["config_detail"] = {"step": "one CUDA-graph replay of the whole graph (captured after warm-up)",
+                             "kernel_variants": "autotuned per layer on the first batch" if ex["tuned"] else
+                             "cost model"}
+    line["e2e"] = {"value": round(e2e_gmacs, 2), "unit": "GMAC/s", "images_per_s": round(images / (e2e_ms / 1e3), 2),
+                   "h2d_bytes_per_step": ex["h2d"], "d2h_bytes_per_step": ex["d2h"], "path": ex["e2e_path"]}
+    line["gpu_launches"] = res["launches"] * args.steps
+    line["clocks"] = clocks
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference_rate(spec, macs_img, budget_s=args.cpu_budget)
+        cb = cpu_reference_rate(spec, macs_img, budget_s=args.cpu_budget)
+        for k in ("images", "seconds"):
+            cb.pop(k, None)
+        if not args.no_numba:
+            nb = reference_numba_rate(spec, macs_img, budget_s=min(args.cpu_budget, 10.0))
+            if nb is not None:
+                cb["reference_numba"] = nb
+        line["cpu_baseline"] = cb
     if args.layers_out:
-        picks = graphs[0].tuning()
-        rows = [{"node": k, "variant": lib_variant_name(picks.get(k, 0)), "ms": round(v[0] / v[2], 4),
-                 "gmacs": round(v[1] / (v[0] / 1e3) / 1e9, 1),
-                 "frac": round(v[1] / (v[0] / 1e3) / peak_lookups, 4)} for k, v in layer_rows.items()]
-        Path(args.layers_out).write_text(json.dumps(rows, indent=1))
+        g0 = ex["graphs"][0]
+        picks = g0.tuning()
+        peak = line["roofline"]["peak"] * 1e9
+        rows = {}
+        for nid, a, b, m, _, _ in ex["profile"]:
+            r = rows.setdefault(nid, [0.0, 0, 0])
+            r[0] += a.elapsed_time(b)
+            r[1] += m
+            r[2] += 1
+        Path(args.layers_out).write_text(json.dumps(
+            [{"node": k, "variant": lib_variant_name(picks.get(k, 0)), "ms": round(v[0] / v[2], 4),
+              "gmacs": round(v[1] / (v[0] / 1e3) / 1e9, 1), "frac": round(v[1] / (v[0] / 1e3) / peak, 4)}
+             for k, v in rows.items()], indent=1))
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    if line["parity"]["status"] == "MISMATCH":
+        sys.exit(3)
 
 
 if __name__ == "__main__":

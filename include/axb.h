@@ -183,7 +183,16 @@ const char *axb_ft_variant_name(int variant);
 int64_t axb_ftable_cm_bytes(int64_t kpad, int64_t coutp);
 int axb_ftable_cm_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
                           const axb_lut *lut, uint32_t *d_ftable, void *stream);
-/* 0: variant v reads the pair-major table (axb_ftable_prepare), 1: the code-major one */
+/* 64-channel code-major layout for the c64_* variants (axb_ft_variant_layout(v) == 2):
+ *   C64[cb][k][a][pr] = W word of channels (cb*64 + 2*pr, cb*64 + 2*pr + 1), pr = 0..31
+ * i.e. 128 contiguous bytes (all 32 banks) per (64-channel block, row, code); 32 KiB per (cb, k).
+ * The kernel's quarter-warp = one pixel reading one whole row: bank-conflict-free for any codes.
+ * axb_ftable_c64_bytes = kpad * coutp * 512 (0 unless coutp % 64 == 0). */
+int64_t axb_ftable_c64_bytes(int64_t kpad, int64_t coutp);
+int axb_ftable_c64_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                           const axb_lut *lut, uint32_t *d_ftable, void *stream);
+/* 0: variant v reads the pair-major table (axb_ftable_prepare), 1: the 32-channel code-major one,
+ * 2: the 64-channel code-major one */
 int axb_ft_variant_layout(int variant);
 int axb_conv_variant_count(void);
 /* Depthwise approximate conv (config 5; the reference has no groups): channel c

@@ -95,6 +95,8 @@ SIGNATURES = {
     "axb_ft_variant_name": (ctypes.c_char_p, [c_int]),
     "axb_ftable_cm_bytes": (c_i64, [c_i64, c_i64]),
     "axb_ftable_cm_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "axb_ftable_c64_bytes": (c_i64, [c_i64, c_i64]),
+    "axb_ftable_c64_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "axb_ft_variant_layout": (c_int, [c_int]),
     "axb_depthwise_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
     "axb_conv_variant_name": (ctypes.c_char_p, [c_int]),
@@ -166,6 +168,8 @@ def kernel_family(variant_name: str) -> str:
         return "lutconv_ft"
     if variant_name.startswith("cm"):
         return "lutconv_ftcm"
+    if variant_name.startswith("c64"):
+        return "lutconv_ftc64"
     if variant_name.startswith("lutconv_"):
         return variant_name
     if variant_name.startswith("depthwise"):

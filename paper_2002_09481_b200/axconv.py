@@ -141,14 +141,15 @@ def torch_axconv2d(
     if acc_out is not None:
         assert acc_out.dtype == torch.int64 and acc_out.shape == out.shape and acc_out.is_contiguous()
     stream = torch.cuda.current_stream(x.device).cuda_stream
-    rc = _lib.load().axb_axconv2d(
-        x.data_ptr(), n, h, w, c, f.data_ptr(), kh, kw, cout,
-        int(geometry.strides[0]), int(geometry.strides[1]),
-        int(geometry.dilations[0]), int(geometry.dilations[1]), pt, pb, pl, pr,
-        float(in_range[0]), float(in_range[1]), float(f_range[0]), float(f_range[1]),
-        _lib.ROUND[_mode_value(round_mode)], _lib.ACC[_mode_value(accumulator)], dl.handle,
-        out.data_ptr(), acc_out.data_ptr() if acc_out is not None else None, stream,
-    )
+    with torch.cuda.device(x.device):  # the library launches and allocates on the current device
+        rc = _lib.load().axb_axconv2d(
+            x.data_ptr(), n, h, w, c, f.data_ptr(), kh, kw, cout,
+            int(geometry.strides[0]), int(geometry.strides[1]),
+            int(geometry.dilations[0]), int(geometry.dilations[1]), pt, pb, pl, pr,
+            float(in_range[0]), float(in_range[1]), float(f_range[0]), float(f_range[1]),
+            _lib.ROUND[_mode_value(round_mode)], _lib.ACC[_mode_value(accumulator)], dl.handle,
+            out.data_ptr(), acc_out.data_ptr() if acc_out is not None else None, stream,
+        )
     _lib.check(rc)
     return out
 

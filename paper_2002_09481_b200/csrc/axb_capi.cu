@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(256) pool4_kernel(const float4 *__restrict__ x
                     if (MAX) {
                         if (r[j] == r[j] && (v[j] > r[j] || v[j] != v[j])) r[j] = v[j];  // np.max, NaN wins
                     } else {
-                        const float q = v[j] != v[j] ? 0.0f : v[j];  // nansum
-                        r[j] = (t0 + u == 0) ? q : __fadd_rn(r[j], q);
+                        // nansum starts from +0.0 (an all -0.0 window sums to +0.0, like numpy)
+                        const float q = v[j] != v[j] ? 0.0f : v[j];
+                        r[j] = __fadd_rn(r[j], q);
                     }
                 }
                 valid += inb[u];
@@ -176,9 +177,8 @@ __global__ void avgpool_kernel(const float *__restrict__ x, int64_t n, int64_t h
         t /= ow;
         const int64_t oy = t % oh;
         const int64_t b = t / oh;
-        float s = 0.0f;
+        float s = 0.0f;  // nansum's +0.0 start (an all -0.0 window gives +0.0, like numpy)
         int64_t valid = 0;
-        bool first = true;
         for (int ky = 0; ky < ph; ++ky) {
             const int64_t iy = oy * sh + ky - pt;
             for (int kx = 0; kx < pw; ++kx) {
@@ -187,8 +187,7 @@ __global__ void avgpool_kernel(const float *__restrict__ x, int64_t n, int64_t h
                 float v = in ? x[((b * h + iy) * w + ix) * c + ci] : 0.0f;
                 if (v != v) v = 0.0f;  // nansum
                 valid += in;
-                s = first ? v : __fadd_rn(s, v);
-                first = false;
+                s = __fadd_rn(s, v);
             }
         }
         const float y = __double2float_rn((double)s / (double)valid);

@@ -603,6 +603,281 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
                  AXB_FLAG_OUT_NONFINITE);
 }
 
+// ---------------------------------------------------------------- 64-channel code-major variant (C64)
+// Same products, laid out C64[cb][k][a][32 pairs]: the 64 channels of block cb at row k and activation
+// code a are 128 contiguous bytes = all 32 banks.  Lanes = (pixel slot ps = lane>>3, octant o = lane&7):
+// one LDS.128 at a*128 + o*16 returns 4 pairs (8 products) of one pixel, and the 8 lanes of a quarter-warp
+// -- the unit the shared memory serves a 128-bit request in -- are ONE pixel reading one whole 128-byte
+// row: every quarter is one wavefront whatever the codes are.  A warp instruction = 4 pixels x 64 channels
+// = 256 products in exactly 4 wavefronts, the shared-memory peak (64 products per wavefront), with no
+// data-dependent bank conflicts (the pair-major and 32-channel layouts lose 30-50% of their wavefronts to
+// conflicts on real activations).  Table bytes staged per product = 512 / BM (BM = WARPS * 4 * J pixels).
+// Registers: a lane holds 8 accumulator words per pixel (J pixels), so the activation codes do not live
+// in registers ahead of use: each warp stages its 32 pixels' next 16-row chunk in its own shared buffer
+// with cp.async (lane L copies pixel L's 16 bytes), lanes read 8 rows per pixel (LDS.64, broadcast over
+// the pixel's 8 lanes), and lane L sums pixel L's codes (S_p, DP4A) -- shuffled to its lanes at the end.
+constexpr int kC64Pairs = 32;                   // channel pairs per 64-channel block
+constexpr int kC64RowWords = 256 * kC64Pairs;   // one (block, row) slice: 256 codes x 32 pairs
+constexpr int kC64RowBytes = kC64RowWords * 4;  // 32 KiB
+__host__ __device__ constexpr int c64_stage_bytes(int KS) { return KS * kC64RowBytes; }
+__host__ __device__ constexpr int c64_codebuf_bytes(int WARPS) { return WARPS * 2 * 32 * 16; }
+__host__ __device__ constexpr int c64_smem(int KS, int ST, int WARPS) {
+    return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS) + kMaxTaps * 4 + 2 * ST * 8;
+}
+
+template <int J, int WARPS, int KS, int ST, bool SGN>
+__global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
+    constexpr int NT = WARPS * 32;
+    constexpr int PXW = 4 * J;        // pixels per warp
+    constexpr int BM = WARPS * PXW;
+    constexpr int BN = 64;
+    constexpr int SPH = 8 / KS;       // stages per 8-row half chunk
+    constexpr uint32_t STAGE_BYTES = c64_stage_bytes(KS);
+    static_assert(PXW == 32, "one staged code row per lane: 32 pixels per warp (J = 8)");
+    static_assert(KS == 1 || KS == 2 || KS == 4, "KS rows per stage: 1, 2 or 4");
+    static_assert(c64_smem(KS, ST, WARPS) + 512 <= 232448, "C64 ring exceeds shared memory");
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *codebuf = smem + ST * STAGE_BYTES;  // [warp][2][32 pixels][16 B]
+    int32_t *tapoff_s = reinterpret_cast<int32_t *>(codebuf + c64_codebuf_bytes(WARPS));
+    uint64_t *full = reinterpret_cast<uint64_t *>(tapoff_s + kMaxTaps);
+    uint64_t *empty = full + ST;
+
+    const int tid = (int)threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int o = lane & 7, ps = lane >> 3;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, WARPS);
+        }
+    }
+    for (int t = tid; t < p.taps; t += NT) tapoff_s[t] = ((t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw) * p.cs;
+    __syncthreads();
+
+    // 32-bit loop state throughout (registers are the budget here; the host guarantees
+    // ntiles * stages-per-tile < 2^31)
+    const int grid = (int)gridDim.x;
+    const int cid = (int)blockIdx.x;
+    const int my_tiles = p.ntiles > cid ? (int)((p.ntiles - cid + grid - 1) / grid) : 0;
+    const int spt = p.nchunks * 2 * SPH;  // stages per tile
+    const int total = my_tiles * spt;
+
+    int pr_h = 0, pr_q = 0, pr_tile = cid, pr_slot = 0;
+    auto produce = [&]() {
+        const int nb = pr_tile / p.ntm;
+        mbar_expect_tx(full + pr_slot, STAGE_BYTES);
+        bulk_g2s(smem + pr_slot * STAGE_BYTES,
+                 p.ftable + ((int64_t)nb * p.kpad + pr_q * KS) * kC64RowWords, STAGE_BYTES, full + pr_slot);
+        ++pr_h;
+        if (++pr_slot == ST) pr_slot = 0;
+        if (++pr_q == spt) {
+            pr_q = 0;
+            pr_tile += grid;
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < ST - 1 && pr_h < total; ++s) produce();
+
+    // ---- code loader: lane L stages pixel L (of this warp's 32) one 16-row chunk ahead
+    uint8_t *wbuf = codebuf + warp * (2 * 32 * 16);
+    int32_t rowbase = 0;  // byte offset of lane L's pixel in the zp-padded code tensor
+    auto set_row = [&](int tile) {
+        const int64_t mt = (int64_t)(tile % p.ntm) * BM + warp * PXW + lane;
+        int64_t pix0 = 0;
+        if (mt < p.M) pixel_of(p, mt, pix0);
+        rowbase = (int32_t)(pix0 * p.cs);
+    };
+    pdl_wait();
+    int ld_t = 0, ld_ci = 0, ld_kc = 0, ld_buf = 0;
+    int ld_left = my_tiles * p.nchunks, ld_tile = cid;
+    auto load_next = [&]() {
+        if (ld_left > 0) {
+            cp_async16(wbuf + ld_buf * 512 + lane * 16, p.codes + rowbase + tapoff_s[ld_t] + ld_ci, 16);
+            --ld_left;
+            ld_ci += 16;
+            if (ld_ci == p.cs) {
+                ld_ci = 0;
+                ++ld_t;
+            }
+            if (++ld_kc == p.nchunks) {
+                ld_kc = ld_t = ld_ci = 0;
+                ld_tile += grid;
+                if (ld_left > 0) set_row(ld_tile);
+            }
+        }
+        ld_buf ^= 1;
+        cp_async_commit();  // one group per chunk (possibly empty), so wait_group<1> tracks chunk c
+    };
+
+    uint32_t acc_all[J][4], acc_hi[J][4];
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc_all[j][r] = acc_hi[j][r] = 0;
+    int32_t spl = 0;  // S_p of lane L's pixel
+    float tmin = INFINITY, tmax = -INFINITY;
+    int nonfinite = 0;
+    const int64_t bias_units = SGN ? (int64_t)32768 * p.kpad : 0;
+
+    int g = 0, slot = 0;
+    uint32_t phase = 0;
+    int c_tile = cid;
+    int cbuf = 0;
+    if (my_tiles > 0) {
+        set_row(c_tile);
+        load_next();
+    }
+    const uint8_t *tab_lane = smem + o * 16;
+    for (int jt = 0; jt < my_tiles; ++jt) {
+#pragma unroll 1
+        for (int kc = 0; kc < p.nchunks; ++kc) {
+            __syncwarp();   // every lane is done reading the buffer the next copy overwrites
+            load_next();    // chunk kc+1 -> the other buffer
+            cp_async_wait<1>();
+            __syncwarp();   // chunk kc of all 32 pixels has landed
+            const uint8_t *cb_ = wbuf + cbuf * 512;
+            {  // S_p of pixel L (axconv.py:193; junk codes are raw 0 -> value 0)
+                const uint4 mine = *reinterpret_cast<const uint4 *>(cb_ + lane * 16);
+                if (SGN) {
+                    spl = __dp4a((int)mine.x, 0x01010101, spl);
+                    spl = __dp4a((int)mine.y, 0x01010101, spl);
+                    spl = __dp4a((int)mine.z, 0x01010101, spl);
+                    spl = __dp4a((int)mine.w, 0x01010101, spl);
+                } else {
+                    uint32_t t = __dp4a(mine.x, 0x01010101u, (uint32_t)spl);
+                    t = __dp4a(mine.y, 0x01010101u, t);
+                    t = __dp4a(mine.z, 0x01010101u, t);
+                    spl = (int32_t)__dp4a(mine.w, 0x01010101u, t);
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                uint2 cur[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) cur[j] = *reinterpret_cast<const uint2 *>(cb_ + (j * 4 + ps) * 16 + hh * 8);
+#pragma unroll
+                for (int st = 0; st < SPH; ++st) {
+                    if (tid == 0 && pr_h < total) {
+                        // refill the slot stage g-1 used once every warp released it
+                        if (g >= 1) {
+                            const int ps_ = slot == 0 ? ST - 1 : slot - 1;
+                            const uint32_t ph_ = slot == 0 ? phase ^ 1u : phase;
+                            mbar_wait(empty + ps_, ph_);
+                        }
+                        produce();
+                    }
+                    mbar_wait(full + slot, phase);
+                    const uint8_t *stab = tab_lane + slot * STAGE_BYTES;
+#pragma unroll
+                    for (int kl = 0; kl < KS; ++kl) {
+                        const int r = st * KS + kl;  // row within the half chunk (compile-time)
+#pragma unroll
+                        for (int j = 0; j < J; ++j) {
+                            const uint32_t a = __byte_perm(r < 4 ? cur[j].x : cur[j].y, 0, 0x4440u + (r & 3));
+                            const uint4 w = *reinterpret_cast<const uint4 *>(stab + kl * kC64RowBytes + a * 128u);
+                            acc_all[j][0] += w.x; acc_hi[j][0] += w.x >> 16;
+                            acc_all[j][1] += w.y; acc_hi[j][1] += w.y >> 16;
+                            acc_all[j][2] += w.z; acc_hi[j][2] += w.z >> 16;
+                            acc_all[j][3] += w.w; acc_hi[j][3] += w.w >> 16;
+                        }
+                    }
+                    fence_proxy_async_smem();  // this lane's LDS reads of the slot before the TMA refill
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + slot);
+                    ++g;
+                    if (++slot == ST) {
+                        slot = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+            cbuf ^= 1;
+        }
+
+        // ------------------------------------------------ fused epilogue (same arithmetic as lutconv_ft)
+        {
+            const EpiConst e = epi_const(p);
+            const int nb = c_tile / p.ntm;
+            const int64_t m0 = (int64_t)(c_tile % p.ntm) * BM;
+            const int cb = nb * BN + o * 8;  // this lane's 8 channels
+            const bool full_blk = cb + 8 <= p.cout && (p.cout & 3) == 0;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int32_t spj = __shfl_sync(0xffffffffu, spl, j * 4 + ps);
+                const int64_t mt = m0 + warp * PXW + j * 4 + ps;
+                if (mt < p.M) {
+                    int64_t pix0;
+                    const int64_t m = pixel_of(p, mt, pix0);
+                    const int64_t pz = -e.zp2 * (int64_t)spj;
+                    float *dst = p.out + m * p.cout + cb;
+#pragma unroll
+                    for (int hq = 0; hq < 2; ++hq) {
+                        int64_t A[4];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t hi = acc_hi[j][2 * hq + h];
+                            const uint32_t lo = acc_all[j][2 * hq + h] - (hi << 16);
+                            A[2 * h] = (int64_t)lo - bias_units;
+                            A[2 * h + 1] = (int64_t)hi - bias_units;
+                        }
+                        const int c0 = cb + 4 * hq;
+                        if (full_blk) {
+                            float y[4];
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254); fp64 dequant (:256)
+                                const int64_t corr = A[t] + pz - e.zp1 * __ldg(p.fsum + c0 + t) + e.kzz;
+                                y[t] = __double2float_rn(e.scale * __ll2double_rn(corr));
+                                if (p.bias) y[t] = __fadd_rn(y[t], __ldg(p.bias + c0 + t));  // graph.py:268-269
+                            }
+                            if (p.residual) {  // graph.py:282-286
+                                const float4 r = __ldg(reinterpret_cast<const float4 *>(p.residual + m * p.cout + c0));
+                                y[0] = __fadd_rn(y[0], r.x); y[1] = __fadd_rn(y[1], r.y);
+                                y[2] = __fadd_rn(y[2], r.z); y[3] = __fadd_rn(y[3], r.w);
+                            }
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                if (p.relu) y[t] = (y[t] > 0.0f || y[t] != y[t]) ? y[t] : 0.0f;  // np.maximum(x, 0)
+                                track(y[t], tmin, tmax, nonfinite);
+                            }
+                            *reinterpret_cast<float4 *>(dst + 4 * hq) = make_float4(y[0], y[1], y[2], y[3]);
+                            if (p.acc_out) {
+#pragma unroll
+                                for (int t = 0; t < 4; ++t) p.acc_out[m * p.cout + c0 + t] = A[t];
+                            }
+                        } else {
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                if (c0 + t < p.cout) {
+                                    const int64_t corr = A[t] + pz - e.zp1 * p.fsum[c0 + t] + e.kzz;
+                                    float v = __double2float_rn(e.scale * __ll2double_rn(corr));
+                                    if (p.bias) v = __fadd_rn(v, p.bias[c0 + t]);
+                                    if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + c0 + t]);
+                                    if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;
+                                    track(v, tmin, tmax, nonfinite);
+                                    dst[4 * hq + t] = v;
+                                    if (p.acc_out) p.acc_out[m * p.cout + c0 + t] = A[t];
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc_all[j][r] = acc_hi[j][r] = 0;
+            }
+            spl = 0;
+        }
+        c_tile += grid;
+    }
+    cp_async_wait<0>();
+    const bool any = tmin <= tmax;
+    range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
+                 AXB_FLAG_OUT_NONFINITE);
+}
+
 // ---------------------------------------------------------------- table preparation
 // W[sb][k][pair][a] = (u(lut[(a<<8)|F[k][c]]), u(lut[(a<<8)|F[k][c+1]])), c = sb*8 + 2*pair (8-channel
 // sub-blocks); u = raw ^ 0x8000 (signed) / raw (unsigned); junk rows (ci >= c or k >= taps*cs) = zero
@@ -655,12 +930,38 @@ __global__ void ftable_cm_kernel(const uint8_t *__restrict__ fcodes, int64_t kpa
     }
 }
 
+// C64[cb][k][a][pr] = W word of channels (cb*64 + 2*pr, +1) at row k, code a (128 B per code and row)
+__global__ void ftable_c64_kernel(const uint8_t *__restrict__ fcodes, int64_t kpad, int64_t coutp, int32_t cs,
+                                  int32_t c, int64_t kreal, const uint16_t *__restrict__ lut_b, int sgn,
+                                  uint32_t *__restrict__ out) {
+    const int64_t total = (coutp / 64) * kpad * kC64RowWords;
+    const uint32_t flip = sgn ? 0x8000u : 0u;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int pr = (int)(idx & 31);
+        const uint32_t a = (uint32_t)((idx >> 5) & 255);
+        const int64_t rest = idx >> 13;
+        const int64_t k = rest % kpad;
+        const int64_t cb = rest / kpad;
+        uint32_t w = flip | (flip << 16);
+        if (k < kreal && (int)(k % cs) < c) {
+            const int64_t col = cb * 64 + 2 * pr;
+            const uint32_t b0 = fcodes[k * coutp + col], b1 = fcodes[k * coutp + col + 1];
+            const uint32_t u0 = (uint32_t)__ldg(lut_b + b0 * 256 + a) ^ flip;
+            const uint32_t u1 = (uint32_t)__ldg(lut_b + b1 * 256 + a) ^ flip;
+            w = u0 | (u1 << 16);
+        }
+        out[idx] = w;
+    }
+}
+
 // ---------------------------------------------------------------- host launch
 struct FtVariant {
     const char *name;
     int tm, warps, npb, cl;
     float cost;  // relative time per lookup slot (1 = best); tuned on B200
-    int cm;      // 1: code-major table (axb_ftable_cm_prepare), tm = J pixels per lane per 8-pixel group
+    int cm;      // 1: code-major 32-channel table (axb_ftable_cm_prepare), tm = J pixels per lane per 8-pixel
+                 // group; 2: code-major 64-channel table (axb_ftable_c64_prepare), tm = J pixels per lane
 };
 static const FtVariant kFtVariants[] = {
     {"auto", 0, 0, 0, 0, 0.f},
@@ -678,6 +979,10 @@ static const FtVariant kFtVariants[] = {
     {"cm32_j8_w8_k4", 8, 8, 16, 1, 1.000f, 1},
     {"cm32_j4_w12_k4", 4, 12, 16, 1, 1.000f, 1},
     {"cm32_j6_w16_k4", 6, 16, 16, 1, 1.000f, 1},
+    {"c64_j8_w16_k2", 8, 16, 32, 1, 1.000f, 2},
+    {"c64_j8_w12_k2", 8, 12, 32, 1, 1.000f, 2},
+    {"c64_j8_w8_k2", 8, 8, 32, 1, 1.000f, 2},
+    {"c64_j8_w16_k1", 8, 16, 32, 1, 1.000f, 2},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
@@ -716,6 +1021,45 @@ static int launch_ftcm(int op, const ConvK &k, int sm_limit, cudaStream_t s, con
     if (cudaLaunchKernelEx(&cfg, fn, kk) != cudaSuccess) return check_launch("lutconv_ftcm");
     set_last_kernel(name);
     return check_launch("lutconv_ftcm");
+}
+
+template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3>
+static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
+    constexpr int BM = WARPS * 4 * J;
+    constexpr int BN = 64;
+    const size_t smem = c64_smem(KS, ST, WARPS);
+    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN>;
+    static int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_ftc64");
+        configured_dev = dev;
+    }
+    if (op == 1) return sm_count();
+    if (k.coutp % BN) return set_error(AXB_E_VALUE, "64-channel code-major kernel needs coutp % 64 == 0");
+    ConvK kk = k;
+    kk.ntm = (int32_t)((k.M + BM - 1) / BM);
+    kk.ntiles = (int64_t)kk.ntm * (k.coutp / BN);
+    if (kk.ntiles * (int64_t)k.nchunks * (16 / KS) >= (int64_t)1 << 31)
+        return set_error(AXB_E_VALUE, "conv too large for the c64 kernel's 32-bit stage counters");
+    int64_t nblk = sm_limit > 0 ? sm_limit : sm_count();
+    if (nblk > kk.ntiles) nblk = kk.ntiles;
+    if (nblk < 1) nblk = 1;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)nblk);
+    cfg.blockDim = dim3(WARPS * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, fn, kk) != cudaSuccess) return check_launch("lutconv_ftc64");
+    set_last_kernel(name);
+    return check_launch("lutconv_ftc64");
 }
 
 // op 0: launch; op 1: return how many CL-CTA clusters fit on the device at once (cached)
@@ -789,6 +1133,10 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 12: return launch_ftcm<8, 8, SGN>(op, k, sm_limit, s, nm);
         case 13: return launch_ftcm<4, 12, SGN>(op, k, sm_limit, s, nm);
         case 14: return launch_ftcm<6, 16, SGN>(op, k, sm_limit, s, nm);
+        case 15: return launch_ftc64<8, 16, SGN>(op, k, sm_limit, s, nm);
+        case 16: return launch_ftc64<8, 12, SGN>(op, k, sm_limit, s, nm);
+        case 17: return launch_ftc64<8, 8, SGN>(op, k, sm_limit, s, nm);
+        case 18: return launch_ftc64<8, 16, SGN, 1, 6>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
@@ -869,6 +1217,28 @@ int axb_ftable_cm_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64
                                                                      kh * kw * cs, lut->d_bmajor, lut->is_signed,
                                                                      d_ftable);
     return check_launch("ftable_cm_prepare");
+}
+
+int64_t axb_ftable_c64_bytes(int64_t kpad, int64_t coutp) {
+    if (kpad <= 0 || coutp <= 0 || kpad % 16 || coutp % 64) return 0;
+    return kpad * (coutp / 64) * kC64RowBytes;
+}
+
+int axb_ftable_c64_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                           const axb_lut *lut, uint32_t *d_ftable, void *stream) {
+    if (!lut || !d_fcodes || !d_ftable) return set_error(AXB_E_VALUE, "null argument");
+    if (cs % 16 || c > cs || c < 1) return set_error(AXB_E_VALUE, "channel stride mismatch");
+    const int64_t kpad = axb_filter_kpad(kh, kw, cs), coutp = axb_filter_coutp(cout);
+    if (coutp % 64) return set_error(AXB_E_VALUE, "64-channel code-major table needs coutp % 64 == 0");
+    const int64_t total = (coutp / 64) * kpad * kC64RowWords;
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    ftable_c64_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_fcodes, kpad, coutp, (int32_t)cs, (int32_t)c,
+                                                                      kh * kw * cs, lut->d_bmajor, lut->is_signed,
+                                                                      d_ftable);
+    return check_launch("ftable_c64_prepare");
 }
 
 int axb_ft_variant_layout(int v) { return (v >= 1 && v < kNumFtVariants) ? kFtVariants[v].cm : 0; }

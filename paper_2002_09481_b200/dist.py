@@ -25,18 +25,28 @@ def shard(n_units: int, world: int, rank: int) -> list[int]:
 
 
 def exchange_results(logits: torch.Tensor, counts: torch.Tensor, times: torch.Tensor, group=None):
-    """All-gather logits (equal shapes per rank), all-reduce counts (SUM) and times (MAX).
+    """All-gather logits, all-reduce counts (SUM) and times (MAX).
 
-    Returns (gathered_logits [world x ...], counts, times); a no-op when
-    torch.distributed is not initialised.
+    ``logits`` is (units, ...) per rank; ranks may hold different numbers of
+    units (a 32-table sweep over 3 ranks: 11/11/10), so the unit counts are
+    gathered first and every rank's block is padded to the largest for the
+    one NCCL all-gather.  Returns (list of per-rank logits, counts, times); a
+    no-op when torch.distributed is not initialised.
     """
     import torch.distributed as dist
 
     if not (dist.is_available() and dist.is_initialized()):
-        return logits.unsqueeze(0), counts, times
+        return [logits], counts, times
     world = dist.get_world_size(group)
-    gathered = [torch.empty_like(logits) for _ in range(world)]
-    dist.all_gather(gathered, logits.contiguous(), group=group)
+    n = torch.tensor([logits.shape[0]], dtype=torch.int64, device=logits.device)
+    sizes = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(v.item()) for v in sizes]
+    top = max(sizes)
+    pad = logits.new_zeros((top,) + tuple(logits.shape[1:]))
+    pad[:logits.shape[0]] = logits
+    gathered = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(gathered, pad.contiguous(), group=group)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(times, op=dist.ReduceOp.MAX, group=group)
-    return torch.stack(gathered), counts, times
+    return [g[:k] for g, k in zip(gathered, sizes)], counts, times

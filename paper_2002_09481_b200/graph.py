@@ -143,7 +143,15 @@ class GpuGraph:
             if n["kind"] == "AxConv2D":
                 if len(n["inputs"]) != 3:
                     raise ValueError(f"AxConv2D node {n['id']!r} needs data, min, and max inputs")
-                conv_plans[n["id"]] = _ConvPlan(node=n, x=n["inputs"][0], out=n["id"])
+                # the executor quantizes with the device range of the data input (graph.py:248-251 reads
+                # whatever the Min/Max inputs computed): they must be Min and Max over that same tensor
+                x, mn, mx = n["inputs"]
+                for rid, want in ((mn, "Min"), (mx, "Max")):
+                    rn = self.by_id[rid]
+                    if rn["kind"] != want or rn.get("inputs", [None])[0] != x:
+                        raise ValueError(f"AxConv2D node {n['id']!r}: range input {rid!r} must be a {want} node "
+                                         f"over its data input {x!r}")
+                conv_plans[n["id"]] = _ConvPlan(node=n, x=x, out=n["id"])
         # Add fusion: pick the later-produced conv operand with a single consumer
         for n in nodes:
             if n["kind"] != "Add":
@@ -268,15 +276,23 @@ class GpuGraph:
 
     # ------------------------------------------------------------------ execution
     def run(self, batch: torch.Tensor, check: bool = True, trace: dict | None = None,
-            profile: list | None = None, timeline: list | None = None) -> torch.Tensor:
+            profile: list | None = None, timeline: list | None = None,
+            mprofile: list | None = None) -> torch.Tensor:
         """Evaluate on a (n,h,w,c) fp32 CUDA batch; returns the last node's value.
 
         ``profile`` (a list) receives (node_id, start_event, end_event, macs, ...)
         around every LUT-conv kernel launch, for live per-kernel timing;
         ``timeline`` (a list) receives (node_id, step_kind, start_event, end_event)
         around every executed node (the GPU counterpart of ``Meter.node``,
-        metering.py:39-46; ``benchmark.run_benchmark`` turns both into a RunReport).
+        metering.py:39-46; ``benchmark.run_benchmark`` turns both into a RunReport);
+        ``mprofile`` (a list) receives (node_id, kernel kind, start_event, end_event,
+        algorithmic HBM bytes) around every memory-bound launch: range, record decode,
+        quantize, pools, add -- for the HBM GB/s of those kernels.
         """
+        with torch.cuda.device(self.device):  # launches and stream-ordered allocations on self.device
+            return self._run(batch, check, trace, profile, timeline, mprofile)
+
+    def _run(self, batch, check, trace, profile, timeline, mprofile) -> torch.Tensor:
         records = batch.dtype == torch.uint8
         if records:  # CIFAR-10 binary records (n, 3073): decoded on the device (formats.py:138-157)
             if batch.dim() != 2 or batch.shape[1] != CIFAR_RECORD_BYTES:
@@ -295,12 +311,25 @@ class GpuGraph:
         self.flags.zero_()
         self.launches = 0  # libaxb kernels launched by this run
         self._profile = profile
+        self._mprofile = mprofile
+
+        def mtime(nid, kind, nbytes, fn):
+            if mprofile is None:
+                return fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = fn()
+            e1.record()
+            mprofile.append((nid, kind, e0, e1, int(nbytes)))
+            return r
         self._codes: dict[str, dict] = {}  # exported code tensors (share_from), alive for this run
         vals: dict[str, torch.Tensor] = {}
+        # uses of each tensor by the steps that actually execute (fused-away Add/ReLU and Min/Max nodes
+        # read nothing at run time), so every intermediate is freed after its last reader
         remaining = {tid: 0 for tid in self.slot}
-        for n in self.nodes:
-            for i in n.get("inputs", []):
-                remaining[self.t(i)] += 1
+        for st in self.steps:
+            for tid in self._step_reads(st):
+                remaining[tid] += 1
         last = None
 
         def rng_ptr(tid):
@@ -309,11 +338,10 @@ class GpuGraph:
         def flag_ptr(tid):
             return self.flags[self.slot[tid]].data_ptr()
 
-        def release(n):
+        def release(st):
             if trace is not None:
                 return
-            for i in n.get("inputs", []):
-                tid = self.t(i)
+            for tid in self._step_reads(st):
                 remaining[tid] -= 1
                 if remaining[tid] == 0 and tid in vals and tid != last:
                     del vals[tid]
@@ -330,8 +358,10 @@ class GpuGraph:
                     self.labels = torch.empty(in_shape[0], dtype=torch.uint8, device=self.device)
                 if in_shape[0] == 0 and nid in self.need_range:
                     raise ValueError("cannot take the range of an empty tensor")
-                _lib.check(lib.axb_cifar_decode(batch.data_ptr(), in_shape[0], images.data_ptr(),
-                                                self.labels.data_ptr(), rng_ptr(nid), flag_ptr(nid), stream))
+                mtime(nid, "cifar_decode", in_shape[0] * (CIFAR_RECORD_BYTES + 3072 * 4 + 1),
+                      lambda: _lib.check(lib.axb_cifar_decode(batch.data_ptr(), in_shape[0], images.data_ptr(),
+                                                              self.labels.data_ptr(), rng_ptr(nid), flag_ptr(nid),
+                                                              stream)))
                 self.launches += 1
                 vals[nid] = images
             elif st.kind == "Input":
@@ -339,8 +369,9 @@ class GpuGraph:
                 if nid in self.need_range:
                     if batch.numel() == 0:
                         raise ValueError("cannot take the range of an empty tensor")
-                    _lib.check(lib.axb_range_minmax(batch.data_ptr(), batch.numel(), rng_ptr(nid),
-                                                    flag_ptr(nid), stream))
+                    mtime(nid, "range", batch.numel() * 4,
+                          lambda: _lib.check(lib.axb_range_minmax(batch.data_ptr(), batch.numel(), rng_ptr(nid),
+                                                                  flag_ptr(nid), stream)))
                     self.launches += 1
             elif st.kind == "conv":
                 vals[nid] = self._run_conv(st.plan, vals, rng_ptr(nid), flag_ptr(nid), stream)
@@ -350,9 +381,10 @@ class GpuGraph:
                 if b is not None and a.shape != b.shape:
                     raise ValueError(f"Add node {nid!r} input shapes differ")
                 out = torch.empty_like(a)
-                _lib.check(lib.axb_add_relu(a.data_ptr(), b.data_ptr() if b is not None else None, a.numel(),
-                                            int(st.kind == "ReLU"), out.data_ptr(), rng_ptr(nid), flag_ptr(nid),
-                                            stream))
+                mtime(nid, "add_relu", a.numel() * 4 * (3 if b is not None else 2),
+                      lambda: _lib.check(lib.axb_add_relu(a.data_ptr(), b.data_ptr() if b is not None else None,
+                                                          a.numel(), int(st.kind == "ReLU"), out.data_ptr(),
+                                                          rng_ptr(nid), flag_ptr(nid), stream)))
                 self.launches += 1
                 vals[nid] = out
             elif st.kind in ("MaxPool", "AvgPool"):
@@ -361,9 +393,10 @@ class GpuGraph:
                 os_ = self.shapes[nid]
                 out = torch.empty(os_, dtype=torch.float32, device=self.device)
                 fn = lib.axb_maxpool if st.kind == "MaxPool" else lib.axb_avgpool
-                _lib.check(fn(x.data_ptr(), *x.shape, e["ph"], e["pw"], e["geo"].strides[0], e["geo"].strides[1],
-                              e["pads"][0], e["pads"][2], os_[1], os_[2], out.data_ptr(), rng_ptr(nid),
-                              flag_ptr(nid), stream))
+                mtime(nid, "pool", (x.numel() + out.numel()) * 4,
+                      lambda: _lib.check(fn(x.data_ptr(), *x.shape, e["ph"], e["pw"], e["geo"].strides[0],
+                                            e["geo"].strides[1], e["pads"][0], e["pads"][2], os_[1], os_[2],
+                                            out.data_ptr(), rng_ptr(nid), flag_ptr(nid), stream)))
                 self.launches += 1
                 vals[nid] = out
             elif st.kind == "Flatten":
@@ -388,7 +421,7 @@ class GpuGraph:
                 ev1.record()
                 timeline.append((nid, st.kind, ev0, ev1))
             last = self.t(nid)
-            release(n)
+            release(st)
         out = vals[last]
         if check:
             self.check_flags()
@@ -399,6 +432,12 @@ class GpuGraph:
         if out.dim() == 2:
             out = out.reshape(out.shape[0], 1, 1, out.shape[1])
         return out
+
+    def _step_reads(self, st) -> list:
+        """Tensor ids a step reads at run time (the conv's data input and fused residual)."""
+        if st.kind == "conv":
+            return [self.t(st.plan.x)] + ([self.t(st.plan.residual)] if st.plan.residual is not None else [])
+        return [self.t(i) for i in st.node.get("inputs", [])]
 
     def autotune(self, batch: torch.Tensor, reps: int = 3) -> dict:
         """Pick each conv layer's kernel by timing every ftable-kernel variant and the b-major LUT
@@ -424,6 +463,12 @@ class GpuGraph:
         for st in self.steps:
             if st.kind == "conv" and st.node["id"] in picks:
                 st.plan.ft_variant = int(picks[st.node["id"]])
+                if st.plan.layer is not None:
+                    st.plan.layer.keep_tables(st.plan.ft_variant)
+
+    def table_bytes(self) -> int:
+        """Device bytes of all resident product tables (filter-specialised, both layouts)."""
+        return sum(st.plan.layer.table_bytes() for st in self.steps if st.kind == "conv" and st.plan.layer)
 
     def copy_tuning(self, other: "GpuGraph") -> None:
         """Adopt another graph's per-layer kernel choices (same architecture, e.g. the candidate
@@ -434,12 +479,18 @@ class GpuGraph:
             raise ValueError("copy_tuning needs graphs of the same architecture")
         for a, b in zip(mine, theirs):
             a.ft_variant = b.ft_variant
+            if a.layer is not None:
+                a.layer.keep_tables(a.ft_variant)
 
     def check_flags(self):
         self._check_flag_array(self.flags.cpu().numpy())
 
     # ------------------------------------------------------------------ CUDA graphs + pipelined host I/O
     def capture(self, in_shape, slots: int = 2, dtype=torch.float32) -> None:
+        with torch.cuda.device(self.device):
+            self._capture(in_shape, slots, dtype)
+
+    def _capture(self, in_shape, slots, dtype) -> None:
         """Record ``run`` for a fixed input shape into ``slots`` CUDA graphs (one per static
         input buffer).  Replays launch the whole step (range, quantize, LUT convs, pools, ...)
         with one CPU call; each slot owns its input buffer, output and flag snapshot, so a
@@ -484,6 +535,10 @@ class GpuGraph:
         return sl is not None
 
     def run_pipelined(self, host_batches, host_outputs=None, before_step=None):
+        with torch.cuda.device(self.device):
+            return self._run_pipelined(host_batches, host_outputs, before_step)
+
+    def _run_pipelined(self, host_batches, host_outputs, before_step):
         """End-to-end over pinned HOST batches: H2D of step i+1 (copy stream) overlaps the
         captured compute of step i; each step's logits and flags come back D2H.  Host batches
         are NHWC fp32 images or (n, 3073) uint8 CIFAR-10 records (decoded on the device).
@@ -535,6 +590,7 @@ class GpuGraph:
     def _check_flag_array(self, fl):
         if fl.any() and (np.asarray(fl) & _lib.FLAG_LABEL).any():
             raise FormatError("label byte outside 0..9")
+
         for n in self.nodes:
             if n["kind"] in ("Min", "Max"):
                 tid = self.t(n["inputs"][0])
@@ -544,6 +600,8 @@ class GpuGraph:
             if n["kind"] == "AxConv2D":
                 if fl[self.slot[self.t(n["id"])]] & _lib.FLAG_PSUM_OVF:
                     raise OverflowError("patch length too large for 32-bit code sums")
+        if fl[len(self.slot)] & _lib.FLAG_NONFINITE:  # the shared quantize flag (quantizer.py:123-124)
+            raise ValueError("cannot quantize non-finite values")
 
     def _run_conv(self, p: _ConvPlan, vals, out_range, out_flag, stream):
         x = vals[self.t(p.x)]
@@ -554,11 +612,10 @@ class GpuGraph:
         shared = self._codes.get(p.share_from) if p.share_from and not self.variant else None
         codes_out = {} if p.exports else None
         in_rng = self.ranges[self.slot[self.t(p.x)]].data_ptr()
-        if self._tune and p.layer.ftable is not None and not self.variant:
+        if self._tune and p.layer.has_ft and not self.variant:
             # re-running the layer is idempotent: same codes, same outputs, same range / flag bits
             best, best_t, ref = 0, float("inf"), None
-            cands = [v for v in range(1, self.lib.axb_ft_variant_count())
-                     if p.layer.ftable_cm is not None or self.lib.axb_ft_variant_layout(v) == 0]
+            cands = [v for v in range(1, self.lib.axb_ft_variant_count()) if p.layer.layout_ok(v)]
             for v in cands + [-1]:
                 evs = []
                 for _ in range(self._tune):
@@ -578,8 +635,12 @@ class GpuGraph:
                 if t < best_t:
                     best, best_t = v, t
             p.ft_variant = best
+            p.layer.keep_tables(best)  # free the table layout the pick does not read
+        qprof = [] if self._mprofile is not None else None
         out = p.layer.run(x, in_rng, profile=prof, ft_variant=max(p.ft_variant, 0), use_ftable=p.ft_variant >= 0,
-                          codes_in=shared if p.ft_variant >= 0 else None, codes_out=codes_out, **kw)
+                          codes_in=shared if p.ft_variant >= 0 else None, codes_out=codes_out, qprofile=qprof, **kw)
+        if qprof:
+            self._mprofile.extend((p.node["id"],) + q for q in qprof)
         if codes_out:
             self._codes[p.node["id"]] = codes_out
         if prof:

@@ -34,8 +34,12 @@ FTABLE_MAX_BYTES = 4 << 30  # per layer (ResNet-50's largest: 4608 x 512 x 512 B
 class ConvLayer:
     def __init__(self, filters, f_range, lut, geometry, bias=None, round_mode="half-away-from-zero",
                  accumulator="exact64", device=None, depthwise=False, ftable=None):
-        self.lib = lib = _lib.load()
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        with torch.cuda.device(self.device):  # uploads and launches on the layer's device
+            self._init(filters, f_range, lut, geometry, bias, round_mode, accumulator, depthwise, ftable)
+
+    def _init(self, filters, f_range, lut, geometry, bias, round_mode, accumulator, depthwise, ftable):
+        self.lib = lib = _lib.load()
         f = np.ascontiguousarray(filters, dtype=np.float32)
         self.depthwise = bool(depthwise)
         if self.depthwise:  # (kh, kw, C, 1) -> the (kh, kw, 1, C) view: one input channel per output channel
@@ -80,27 +84,91 @@ class ConvLayer:
         if ftable is None:
             ftable = os.environ.get("AXB_FTABLE", "1") != "0"
         nbytes = int(lib.axb_ftable_bytes(self.kpad, self.coutp))
-        self.ftable = None
-        if ftable and not self.depthwise and nbytes and self.kpad <= 32768 and fk[0] * fk[1] <= 256 \
-                and nbytes <= FTABLE_MAX_BYTES:
-            self.ftable = torch.empty(nbytes // 4, dtype=torch.int32, device=self.device)
-            _lib.check(lib.axb_ftable_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3], self.cout,
-                                              self.lut.handle, self.ftable.data_ptr(), stream))
-        # the same words code-major (cm32_* variants: 8 products per LDS.128) when channels come in 32s
-        cm_bytes = int(lib.axb_ftable_cm_bytes(self.kpad, self.coutp)) if self.ftable is not None else 0
-        self.ftable_cm = None
-        if cm_bytes and cm_bytes <= FTABLE_MAX_BYTES and os.environ.get("AXB_FTABLE_CM", "1") != "0":
-            self.ftable_cm = torch.empty(cm_bytes // 4, dtype=torch.int32, device=self.device)
-            _lib.check(lib.axb_ftable_cm_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3], self.cout,
-                                                 self.lut.handle, self.ftable_cm.data_ptr(), stream))
+        self.has_ft = bool(ftable and not self.depthwise and nbytes and self.kpad <= 32768 and fk[0] * fk[1] <= 256
+                           and nbytes <= FTABLE_MAX_BYTES)
+        # the same words code-major (cm32_* variants: 8 products per LDS.128) when channels come in 32s;
+        # each layout is built on first use and ``keep_tables`` frees the one the layer's kernel does not read
+        cm_bytes = int(lib.axb_ftable_cm_bytes(self.kpad, self.coutp)) if self.has_ft else 0
+        self.cm_ok = bool(cm_bytes and cm_bytes <= FTABLE_MAX_BYTES and os.environ.get("AXB_FTABLE_CM", "1") != "0")
+        # and 64-channel code-major (c64_* variants: bank-conflict-free LDS.128) when channels come in 64s
+        c64_bytes = int(lib.axb_ftable_c64_bytes(self.kpad, self.coutp)) if self.has_ft else 0
+        self.c64_ok = bool(c64_bytes and c64_bytes <= FTABLE_MAX_BYTES
+                           and os.environ.get("AXB_FTABLE_C64", "1") != "0")
+        self.ftable = self.ftable_cm = self.ftable_c64 = None
+        if self.has_ft:
+            self.pair_table()
         self.launches = 0
+
+    def pair_table(self) -> torch.Tensor:
+        """The pair-major product table W[sb][k][pair][a] (axb_ftable_prepare), built on first use."""
+        if self.ftable is None:
+            if not self.has_ft:
+                raise ValueError("this layer has no filter-specialised table")
+            fk = self.f_geom
+            self.ftable = torch.empty(int(self.lib.axb_ftable_bytes(self.kpad, self.coutp)) // 4, dtype=torch.int32,
+                                      device=self.device)
+            with torch.cuda.device(self.device):
+                _lib.check(self.lib.axb_ftable_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3], self.cout,
+                                                       self.lut.handle, self.ftable.data_ptr(),
+                                                       torch.cuda.current_stream(self.device).cuda_stream))
+        return self.ftable
+
+    def cm_table(self) -> torch.Tensor:
+        """The code-major product table CM[cb][k][a][pair] (axb_ftable_cm_prepare), built on first use."""
+        if self.ftable_cm is None:
+            if not self.cm_ok:
+                raise ValueError("code-major ftable variant needs a code-major table (coutp % 32 == 0)")
+            fk = self.f_geom
+            self.ftable_cm = torch.empty(int(self.lib.axb_ftable_cm_bytes(self.kpad, self.coutp)) // 4,
+                                         dtype=torch.int32, device=self.device)
+            with torch.cuda.device(self.device):
+                _lib.check(self.lib.axb_ftable_cm_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3],
+                                                          self.cout, self.lut.handle, self.ftable_cm.data_ptr(),
+                                                          torch.cuda.current_stream(self.device).cuda_stream))
+        return self.ftable_cm
+
+    def c64_table(self) -> torch.Tensor:
+        """The 64-channel code-major table C64[cb][k][a][pair] (axb_ftable_c64_prepare), built on first use."""
+        if self.ftable_c64 is None:
+            if not self.c64_ok:
+                raise ValueError("c64 ftable variant needs a 64-channel code-major table (coutp % 64 == 0)")
+            fk = self.f_geom
+            self.ftable_c64 = torch.empty(int(self.lib.axb_ftable_c64_bytes(self.kpad, self.coutp)) // 4,
+                                          dtype=torch.int32, device=self.device)
+            with torch.cuda.device(self.device):
+                _lib.check(self.lib.axb_ftable_c64_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3],
+                                                           self.cout, self.lut.handle, self.ftable_c64.data_ptr(),
+                                                           torch.cuda.current_stream(self.device).cuda_stream))
+        return self.ftable_c64
+
+    def layout_ok(self, ft_variant: int) -> bool:
+        """Whether this layer can run ftable variant ``ft_variant`` (its table layout fits the channels)."""
+        lay = self.lib.axb_ft_variant_layout(int(ft_variant)) if ft_variant > 0 else 0
+        return self.has_ft and (lay == 0 or (lay == 1 and self.cm_ok) or (lay == 2 and self.c64_ok))
+
+    def keep_tables(self, ft_variant: int) -> None:
+        """Free the product-table layouts the chosen kernel does not read (0 / pair-major variants keep
+        the pair-major table, code-major variants their own layout, -1 -- the b-major LUT kernel --
+        none).  A later different choice rebuilds what it needs."""
+        v = int(ft_variant)
+        lay = self.lib.axb_ft_variant_layout(v) if v > 0 else (0 if v == 0 else -1)
+        if lay != 0:
+            self.ftable = None
+        if lay != 1:
+            self.ftable_cm = None
+        if lay != 2:
+            self.ftable_c64 = None
+
+    def table_bytes(self) -> int:
+        """Device bytes held by this layer's product tables."""
+        return sum(t.numel() * 4 for t in (self.ftable, self.ftable_cm, self.ftable_c64) if t is not None)
 
     def shares_codes_with(self, other: "ConvLayer") -> bool:
         """True when this layer can read ``other``'s code tensor of the same input instead of quantizing
         it again: a 1x1 layer without padding on the ftable kernel, same channels, signedness and rounding
         (same range -> identical codes and coefficients; quantizer.py:98-131)."""
         return (self.kh == self.kw == 1 and not self.kp and not self.depthwise and not other.kp
-                and not other.depthwise and self.ftable is not None and self.cin == other.cin
+                and not other.depthwise and self.has_ft and self.cin == other.cin
                 and self.sgn == other.sgn and self.round == other.round
                 and tuple(self.geometry.dilations) == (1, 1))
 
@@ -114,14 +182,24 @@ class ConvLayer:
     def run(self, x: torch.Tensor, in_range_dev=None, *, relu=False, residual=None, out_range=None,
             out_flag=None, quant_flag=None, acc_out=None, force_generic=False, sm_limit=0, variant=0,
             pixel_order=0, profile=None, ft_variant=0, use_ftable=True, codes_in=None,
-            codes_out=None) -> torch.Tensor:
+            codes_out=None, qprofile=None) -> torch.Tensor:
+        with torch.cuda.device(self.device):
+            return self._run(x, in_range_dev, relu, residual, out_range, out_flag, quant_flag, acc_out,
+                             force_generic, sm_limit, variant, pixel_order, profile, ft_variant, use_ftable,
+                             codes_in, codes_out, qprofile)
+
+    def _run(self, x, in_range_dev, relu, residual, out_range, out_flag, quant_flag, acc_out, force_generic,
+             sm_limit, variant, pixel_order, profile, ft_variant, use_ftable, codes_in, codes_out,
+             qprofile) -> torch.Tensor:
         """x: (n,h,w,cin) fp32 CUDA.  in_range_dev: device int32[2] ordered-float range, or None if
         set_input_params() was called.  Returns (n,oh,ow,cout) fp32.
 
         ``codes_out`` (a dict) receives this call's zp-padded code tensor and its quantization
         parameters; ``codes_in`` (such a dict, from another layer quantizing the SAME tensor with the
         same range, signedness and rounding) lets a 1x1 unpadded layer on the ftable kernel skip its
-        own quantize pass and read the interior of that tensor (``shares_codes_with``)."""
+        own quantize pass and read the interior of that tensor (``shares_codes_with``).
+        ``qprofile`` (a list) receives (kernel kind, start_event, end_event, algorithmic HBM bytes)
+        around the quantize launch."""
         lib = self.lib
         n, h, w, c = (int(v) for v in x.shape)
         if c != (self.cout if self.depthwise else self.cin):
@@ -141,18 +219,29 @@ class ConvLayer:
         self.launches = 0
         qflag = quant_flag if quant_flag is not None else out_flag
         d = _lib.ConvDesc()
+
+        def qtimed(kind, nbytes, fn):
+            if qprofile is None:
+                return fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            qprofile.append((kind, e0, e1, int(nbytes)))
+
         if self.kp:  # small-c layer: quantize + zp-pad + im2col in one pass into kp-byte code rows
             codes = torch.empty(n * oh * ow * self.kp, dtype=torch.uint8, device=self.device)
             pixsum = torch.empty(n * oh * ow, dtype=torch.int32, device=self.device)
-            _lib.check(lib.axb_quantize_im2col(x.data_ptr(), n, h, w, c, pt, pl, self.kh, self.kw, g.strides[0],
-                                               g.strides[1], g.dilations[0], g.dilations[1], oh, ow, self.kp,
-                                               in_range_dev, self.params[0].data_ptr(), self.sgn, self.round,
-                                               codes.data_ptr(), pixsum.data_ptr(), qflag, stream))
+            qtimed("quantize_im2col", x.numel() * 4 + codes.numel() + pixsum.numel() * 4,
+                   lambda: _lib.check(lib.axb_quantize_im2col(
+                       x.data_ptr(), n, h, w, c, pt, pl, self.kh, self.kw, g.strides[0], g.strides[1],
+                       g.dilations[0], g.dilations[1], oh, ow, self.kp, in_range_dev, self.params[0].data_ptr(),
+                       self.sgn, self.round, codes.data_ptr(), pixsum.data_ptr(), qflag, stream)))
             self.launches += 1
             d.n, d.hp, d.wp, d.cs, d.c = n, oh, ow, self.kp, self.kh * self.kw * c
             d.kh = d.kw = d.sh = d.sw = d.dh = d.dw = 1
         elif codes_in is not None:  # read another layer's code tensor: interior pixel (y, x) at (y+pt, x+pl)
-            if not (self.ftable is not None and use_ftable and not variant and not force_generic
+            if not (self.has_ft and use_ftable and not variant and not force_generic
                     and (pt, pb, pl, pr) == (0, 0, 0, 0) and self.kh == self.kw == 1 and codes_in["cs"] == in_cs
                     and codes_in["n"] == n and codes_in["h"] == h and codes_in["w"] == w):
                 raise ValueError("shared code tensor does not fit this layer")
@@ -164,17 +253,18 @@ class ConvLayer:
         else:
             codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
             # the ftable kernel sums patch codes in its loop; only the LUT / generic kernels read pixsum
-            ft = self.ftable is not None and use_ftable and not variant and not force_generic
+            ft = self.has_ft and use_ftable and not variant and not force_generic
             pixsum = None if ft else torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
             pix_ptr = pixsum.data_ptr() if pixsum is not None else None
+            qbytes = x.numel() * 4 + codes.numel() + (pixsum.numel() * 4 if pixsum is not None else 0)
             if in_range_dev is not None:  # coefficients of the device range computed inside the quantize kernel
-                _lib.check(lib.axb_quantize_pad_range(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, in_range_dev,
-                                                      self.sgn, self.round, self.params[0].data_ptr(),
-                                                      codes.data_ptr(), pix_ptr, qflag, stream))
+                qtimed("quantize", qbytes, lambda: _lib.check(lib.axb_quantize_pad_range(
+                    x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, in_range_dev, self.sgn, self.round,
+                    self.params[0].data_ptr(), codes.data_ptr(), pix_ptr, qflag, stream)))
             else:
-                _lib.check(lib.axb_quantize_pad(x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs,
-                                                self.params[0].data_ptr(), self.sgn, self.round, codes.data_ptr(),
-                                                pix_ptr, qflag, stream))
+                qtimed("quantize", qbytes, lambda: _lib.check(lib.axb_quantize_pad(
+                    x.data_ptr(), n, h, w, c, pt, pb, pl, pr, in_cs, self.params[0].data_ptr(), self.sgn,
+                    self.round, codes.data_ptr(), pix_ptr, qflag, stream)))
             self.launches += 1
             d.n, d.hp, d.wp, d.cs, d.c = n, hp_, wp_, in_cs, c
             d.kh, d.kw = self.kh, self.kw
@@ -206,11 +296,11 @@ class ConvLayer:
         d.sm_limit = int(sm_limit)
         d.variant = int(variant)
         d.pixel_order = int(pixel_order)
-        d.ftable = self.ftable.data_ptr() if (self.ftable is not None and use_ftable) else None
-        if d.ftable is not None and ft_variant and lib.axb_ft_variant_layout(int(ft_variant)) == 1:
-            if self.ftable_cm is None:
-                raise ValueError("code-major ftable variant needs a code-major table (coutp % 32 == 0)")
-            d.ftable = self.ftable_cm.data_ptr()
+        table = None
+        if self.has_ft and use_ftable:
+            lay = lib.axb_ft_variant_layout(int(ft_variant)) if ft_variant else 0
+            table = self.cm_table() if lay == 1 else (self.c64_table() if lay == 2 else self.pair_table())
+        d.ftable = table.data_ptr() if table is not None else None
         d.ft_variant = int(ft_variant)
         if profile is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -225,7 +315,7 @@ class ConvLayer:
             # algorithmic HBM bytes of the conv launch: codes (+ per-pixel sums), filter codes or the
             # filter-specialised product table (read once), fp32 output, residual read
             ft = d.ftable is not None
-            algo = d.n * d.hp * d.wp * (d.cs + 4) + (self.ftable.numel() * 4 if ft else self.kpad * self.coutp) \
+            algo = d.n * d.hp * d.wp * (d.cs + 4) + (table.numel() * 4 if ft else self.kpad * self.coutp) \
                 + n * oh * ow * self.cout * (8 if residual is not None else 4)
             profile.append((e0, e1, n * oh * ow * self.kh * self.kw * c * self.cout, algo,
                             _lib.kernel_family(_lib.last_kernel())))

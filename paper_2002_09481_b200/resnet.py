@@ -14,7 +14,17 @@ graph.py:295, which is not reproducible).
 Nodes are plain dicts ``{"id", "kind", "inputs", "attrs"}``; ``to_reference``
 in the tests converts them to ``axemu.graph.Node`` for the real reference.
 
-Weights are synthetic: He-normal filters, N(0, 0.05) biases, from a seed.
+Weights are synthetic: He-normal filters and N(0, 0.05) biases from a seed,
+then **calibrated** (``apply_calibration``).  A BatchNorm is folded into every
+conv: one power-of-two filter scale per layer and one bias per output channel.
+They were measured on the approximate network itself by the real reference
+(``scripts/make_calibration.py``, a fixed calibration batch) and committed in
+``calib.npz``, keyed by architecture, seed and multiplier: a network uses the
+calibration for its own table when one exists, else the one for
+truncated_lut(signed, 2), the benchmark multiplier.  Each conv's output then has roughly
+unit variance and per-channel zero mean, and so do the classifier's logits.
+Without this, the un-normalised He-normal nets predict one class for every
+image (every golden net did in round 1).
 """
 
 from __future__ import annotations
@@ -48,7 +58,64 @@ class _Builder:
         return nid
 
 
-def cifar_resnet(n: int, lut, seed: int = 0, width: int = 16, classes: int = 10) -> list[dict]:
+# ---------------------------------------------------------------------------- calibration
+
+_CALIB_SEED = 424242
+_CALIB_FILE = __import__("pathlib").Path(__file__).with_name("calib.npz")
+_CALIB = None
+
+
+def lut_tag(lut) -> str:
+    """Short content tag of a truth table (signedness + sha256 prefix of the entries)."""
+    import hashlib
+
+    m = getattr(lut.mode, "value", lut.mode)
+    return f"{m[0]}{hashlib.sha256(np.ascontiguousarray(lut.entries).tobytes()).hexdigest()[:10]}"
+
+
+def _calib():
+    global _CALIB
+    if _CALIB is None:
+        _CALIB = dict(np.load(_CALIB_FILE)) if _CALIB_FILE.exists() else {}
+    return _CALIB
+
+
+def calibration_key(arch_seed: str, lut) -> str:
+    """The committed calibration for this network and multiplier, else the one for the benchmark
+    multiplier truncated_lut(signed, 2): a network calibrated once and evaluated with other candidate
+    multipliers (the sweep of config 4)."""
+    from .types import Signedness, truncated_lut
+
+    cal = _calib()
+    own = f"{arch_seed}_{lut_tag(lut)}"
+    if any(k.startswith(own + "/") for k in cal):
+        return own
+    return f"{arch_seed}_{lut_tag(truncated_lut(Signedness.SIGNED, 2))}"
+
+
+def apply_calibration(nodes, key: str) -> list[dict]:
+    """Fold the committed calibration ``key`` (``scripts/make_calibration.py``) into the convs, in place.
+
+    Per conv: filters *= 2^exp (exact in fp32), bias = the calibrated per-channel bias; f_min / f_max
+    follow the filters (transform folds the filter range to constants, graph.py:129-130).
+    """
+    cal = _calib()
+    for nd in nodes:
+        if nd["kind"] != "AxConv2D":
+            continue
+        ek, bk = f"{key}/{nd['id']}/exp", f"{key}/{nd['id']}/bias"
+        if ek not in cal:
+            raise KeyError(f"no calibration {key!r} for conv {nd['id']!r} (scripts/make_calibration.py); "
+                           "build the network with calibrated=False")
+        a = nd["attrs"]
+        f = (a["filters"] * np.float32(2.0 ** int(cal[ek]))).astype(np.float32)
+        a["filters"], a["bias"] = f, cal[bk].astype(np.float32)
+        a["f_min"], a["f_max"] = float(f.min()), float(f.max())
+    return nodes
+
+
+def cifar_resnet(n: int, lut, seed: int = 0, width: int = 16, classes: int = 10,
+                 calibrated: bool = True) -> list[dict]:
     """He et al. 6n+2 CIFAR ResNet (n=1: ResNet-8, n=10: ResNet-62), 32x32x3 input.
 
     Projection (1x1, stride 2) shortcuts where the shape changes.
@@ -69,10 +136,12 @@ def cifar_resnet(n: int, lut, seed: int = 0, width: int = 16, classes: int = 10)
             cin = cout
     g.add("pool", "AvgPool", [x], pool=(8, 8), strides=(8, 8))
     g.conv("fc", "pool", cin, classes, 1)
+    if calibrated:
+        apply_calibration(g.nodes, calibration_key(f"cifar{n}_s{seed}", lut))
     return g.nodes
 
 
-def resnet50(lut, seed: int = 0, classes: int = 1000) -> list[dict]:
+def resnet50(lut, seed: int = 0, classes: int = 1000, calibrated: bool = True) -> list[dict]:
     """ImageNet ResNet-50 (v1.5: stride on the 3x3), 224x224x3 input, 53 convs + 1x1 classifier."""
     g = _Builder(seed, lut)
     g.add("in", "Input", shape=(224, 224, 3))
@@ -93,6 +162,8 @@ def resnet50(lut, seed: int = 0, classes: int = 1000) -> list[dict]:
             cin = cout
     g.add("pool", "AvgPool", [x], pool=(7, 7), strides=(7, 7))
     g.conv("fc", "pool", cin, classes, 1)
+    if calibrated:
+        apply_calibration(g.nodes, calibration_key(f"r50_s{seed}", lut))
     return g.nodes
 
 

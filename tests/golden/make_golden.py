@@ -16,9 +16,13 @@ Fixtures:
              (:131-152), asymmetric same padding (:331-342), config 1, the
              1000-image first layer (sha256 of the output, :225-237),
              quantizer coefficients/codes.
-  nets.npz   end-to-end logits (and per-conv output sha256) of our ResNet-8 /
-             ResNet-62 / ResNet-50 graphs run through the reference
-             ``graph.run`` (engine "gemm").
+  nets.npz   end-to-end logits (and per-conv output sha256) of our calibrated
+             ResNet-8 / ResNet-62 / ResNet-50 graphs run through the reference
+             ``graph.run`` (engine "gemm") on small batches (``--nets``).
+  bench.npz  the benchmarked configurations at full batch, rank 0's bench.py
+             batch: ResNet-8 b1024 and ResNet-50 224x224 b256 with
+             truncated_lut(signed, 2); logits + argmax + per-conv sha256, inputs
+             regenerated from seeds (``--bench [r8] [r50]``, ~7 min).
   formats.npz  bytes the reference's axemu.formats writes / decodes: .axm sha256s,
              a .axt file, a 6-record CIFAR-10 file + its decoded images/labels,
              a report CSV (``--formats`` regenerates only this one).
@@ -220,8 +224,8 @@ def make_nets() -> dict:
         ("r8_trunc2", resnet.cifar_resnet(1, T.truncated_lut(T.Signedness.SIGNED, 2), seed=0), "cifar", 16),
         ("r8_random", resnet.cifar_resnet(1, rl, seed=0), "cifar", 16),
         ("r8_unsigned", resnet.cifar_resnet(1, T.truncated_lut(T.Signedness.UNSIGNED, 1), seed=3), "cifar", 8),
-        ("r62_trunc3", resnet.cifar_resnet(10, T.truncated_lut(T.Signedness.SIGNED, 3), seed=1), "cifar", 4),
-        ("r50_exact", resnet.resnet50(T.exact_lut(T.Signedness.SIGNED), seed=0), "imagenet", 2),
+        ("r62_trunc3", resnet.cifar_resnet(10, T.truncated_lut(T.Signedness.SIGNED, 3), seed=1), "cifar", 32),
+        ("r50_exact", resnet.resnet50(T.exact_lut(T.Signedness.SIGNED), seed=0), "imagenet", 4),
     ]
     out["random_lut_seed123"] = rl.entries
     for tag, nodes, kind, n in runs:
@@ -230,19 +234,54 @@ def make_nets() -> dict:
 
             x, labels = synthetic_cifar10(n, seed=5)
         else:
-            x = np.random.default_rng(2).uniform(0, 1, (n, 224, 224, 3)).astype(np.float32)
-            labels = np.zeros(n, np.uint8)
-        g = to_reference_graph(nodes)
-        trace = {}
-        y = axemu.run(g, Tensor4(x, Layout.NHWC), "gemm", trace=trace).data
+            from paper_2002_09481_b200.datasets import synthetic_imagenet
+
+            x, _ = synthetic_imagenet(n, seed=2)
         out[f"{tag}_x"] = x
-        out[f"{tag}_logits"] = y
-        out[f"{tag}_argmax"] = y.reshape(n, -1).argmax(1)
-        conv_ids = [nd["id"] for nd in nodes if nd["kind"] == "AxConv2D"]
-        out[f"{tag}_conv_ids"] = np.array(conv_ids)
-        out[f"{tag}_conv_sha"] = np.stack(
-            [np.frombuffer(bytes.fromhex(sha(np.asarray(trace[c], np.float32))), np.uint8) for c in conv_ids])
-        print(tag, "argmax", out[f"{tag}_argmax"][:8], flush=True)
+        run_reference(tag, nodes, x, out)
+    return out
+
+
+def run_reference(tag, nodes, x, out):
+    """Logits, argmax and per-conv output sha256 of ``nodes`` on ``x`` through the reference graph.run."""
+    g = to_reference_graph(nodes)
+    trace = {}
+    y = axemu.run(g, Tensor4(x, Layout.NHWC), "gemm", trace=trace).data
+    n = x.shape[0]
+    out[f"{tag}_logits"] = y
+    out[f"{tag}_argmax"] = y.reshape(n, -1).argmax(1)
+    out[f"{tag}_logits_sha"] = np.frombuffer(bytes.fromhex(sha(y)), np.uint8)
+    conv_ids = [nd["id"] for nd in nodes if nd["kind"] == "AxConv2D"]
+    out[f"{tag}_conv_ids"] = np.array(conv_ids)
+    out[f"{tag}_conv_sha"] = np.stack(
+        [np.frombuffer(bytes.fromhex(sha(np.asarray(trace[c], np.float32))), np.uint8) for c in conv_ids])
+    am = out[f"{tag}_argmax"]
+    print(tag, "argmax", am[:16], "distinct", len(set(am.tolist())), flush=True)
+
+
+BENCH_SEED = 1000  # bench.py: rank r's batch is seeded 1000 + r
+
+
+def make_bench() -> dict:
+    """The benchmarked configurations at their full batch (BASELINE configs 2 and 3), rank 0's batch of
+    bench.py: ResNet-8 b1024 (synthetic_cifar10(1024, 1000)) and ResNet-50 224 b256
+    (synthetic_imagenet(256, 1000)), both with truncated_lut(signed, 2).  Inputs are NOT stored (the
+    GPU test and bench.py regenerate them from the seed); logits, argmax and per-conv sha256 are."""
+    from paper_2002_09481_b200 import datasets, resnet
+    from paper_2002_09481_b200 import types as T
+
+    lut = T.truncated_lut(T.Signedness.SIGNED, 2)
+    out = {}
+    which = [a for a in sys.argv[1:] if a in ("r8", "r50")] or ["r8", "r50"]
+    path = HERE / "bench.npz"
+    if path.exists():
+        out.update(dict(np.load(path)))
+    if "r8" in which:
+        x, _ = datasets.synthetic_cifar10(1024, seed=BENCH_SEED)
+        run_reference("r8", resnet.cifar_resnet(1, lut, seed=0), x, out)
+    if "r50" in which:
+        x, _ = datasets.synthetic_imagenet(256, seed=BENCH_SEED)
+        run_reference("r50", resnet.resnet50(lut, seed=0), x, out)
     return out
 
 
@@ -296,6 +335,14 @@ def model_graph_reference(Node, NodeKind):
 
 
 def main():
+    if "--bench" in sys.argv:
+        np.savez_compressed(HERE / "bench.npz", **make_bench())
+        print("bench ok", flush=True)
+        return
+    if "--nets" in sys.argv:
+        np.savez_compressed(HERE / "nets.npz", **make_nets())
+        print("nets ok", flush=True)
+        return
     if "--formats" in sys.argv:
         np.savez_compressed(HERE / "formats.npz", **make_formats())
         print("formats ok", flush=True)

@@ -24,11 +24,12 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     units = shard(10, world, rank)
-    logits = torch.full((4, 3), float(rank)) + torch.arange(3.0)
+    # one (units, 3) logits block per rank; shard(10, 3, r) is uneven: 4 / 3 / 3 units
+    logits = torch.full((len(units), 3), float(rank)) + torch.arange(3.0)
     counts = torch.tensor([rank + 1, 4], dtype=torch.int64)
     times = torch.tensor([10.0 * (rank + 1), 1.0], dtype=torch.float64)
     g, c, t = exchange_results(logits, counts, times)
-    q.put((rank, units, g.tolist(), c.tolist(), t.tolist()))
+    q.put((rank, units, [x.tolist() for x in g], c.tolist(), t.tolist()))
     dist.destroy_process_group()
 
 
@@ -40,11 +41,12 @@ def test_shard_round_robin_covers_all_units_once():
         shard(4, 2, 2)
 
 
-def test_exchange_results_two_ranks_gloo():
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_results_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=120) for _ in procs)
@@ -52,13 +54,16 @@ def test_exchange_results_two_ranks_gloo():
         p.join(timeout=60)
         assert p.exitcode == 0
     for rank, units, g, c, t in res:
-        assert units == list(range(rank, 10, 2))
-        assert len(g) == 2 and g[0][0] == [0.0, 1.0, 2.0] and g[1][0] == [1.0, 2.0, 3.0]
-        assert c == [3, 8]
-        assert t == [20.0, 1.0]
+        assert units == list(range(rank, 10, world))
+        assert len(g) == world
+        for r in range(world):  # every rank's block, trimmed to its own unit count
+            assert len(g[r]) == len(range(r, 10, world))
+            assert all(row == [float(r), r + 1.0, r + 2.0] for row in g[r])
+        assert c == [sum(range(1, world + 1)), 4 * world]
+        assert t == [10.0 * world, 1.0]
 
 
 def test_exchange_is_noop_single_process():
     lg = torch.zeros(2, 3)
     g, c, t = exchange_results(lg, torch.tensor([1]), torch.tensor([2.0]))
-    assert g.shape == (1, 2, 3) and c.tolist() == [1] and t.tolist() == [2.0]
+    assert len(g) == 1 and g[0].shape == (2, 3) and c.tolist() == [1] and t.tolist() == [2.0]

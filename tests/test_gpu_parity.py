@@ -96,13 +96,14 @@ def test_all_ftable_variants_bit_identical():
         want, want_acc = oracle_conv(case, return_acc=True)
         coutp = -(-case["f"].shape[3] // 16) * 16
         for v in range(1, nvar):
-            if lib.axb_ft_variant_layout(v) == 1 and coutp % 32:  # code-major: 32-channel blocks only
+            lay = lib.axb_ft_variant_layout(v)
+            if (lay == 1 and coutp % 32) or (lay == 2 and coutp % 64):  # code-major: 32 / 64-channel blocks
                 continue
-            cm_runs += lib.axb_ft_variant_layout(v)
+            cm_runs += lay > 0
             y, acc, kern = gpu_conv(case, ft_variant=v)
             assert bits_equal(y, want), (v, kern)
             assert np.array_equal(acc, want_acc), (v, kern)
-    assert cm_runs >= 8
+    assert cm_runs >= 12
 
 
 def test_all_tile_variants_bit_identical():
@@ -336,19 +337,63 @@ def test_graph_end_to_end_bit_exact(tag, arch, depth, seed, kind):
     assert np.array_equal(y.reshape(y.shape[0], -1).argmax(1), g[f"{tag}_argmax"])
 
 
-def test_graph_determinism_r50_full_batch():
-    """ResNet-50 at 256 images: identical bits across runs and persistent-grid sizes."""
-    torch = _torch()
-    from paper_2002_09481_b200 import resnet
+def _bench_config(arch):
+    from paper_2002_09481_b200 import datasets, resnet
     from paper_2002_09481_b200 import types as T
-    from paper_2002_09481_b200.graph import GpuGraph
 
     lut = T.truncated_lut(T.Signedness.SIGNED, 2)
-    nodes = resnet.resnet50(lut, seed=0)
-    x = torch.rand((64, 224, 224, 3), generator=torch.Generator().manual_seed(0)).cuda()
-    y1 = GpuGraph(nodes).run(x)
-    y2 = GpuGraph(nodes, sm_limit=100).run(x)
-    assert torch.equal(y1.view(torch.int32), y2.view(torch.int32))
+    if arch == "r8":  # BASELINE config 2, bench.py --workload r8, rank 0's batch
+        return resnet.cifar_resnet(1, lut, seed=0), datasets.synthetic_cifar10(1024, seed=1000)[0]
+    return resnet.resnet50(lut, seed=0), datasets.synthetic_imagenet(256, seed=1000)[0]  # config 3 (default)
+
+
+def _sha(t) -> bytes:
+    return hashlib.sha256(np.ascontiguousarray(t.cpu().numpy()).tobytes()).digest()
+
+
+@pytest.mark.parametrize("arch", ["r8", "r50"])
+def test_benchmarked_configs_bit_exact_vs_reference(arch):
+    """The benchmarked networks at their full batch -- ResNet-8 b1024 and ResNet-50 224x224 b256 with
+    truncated_lut(signed, 2), calibrated weights -- against the REAL reference graph.run on the same
+    batch (tests/golden/bench.npz): every unfused conv output, all logits, argmax.  Then again after the
+    per-layer autotune, through the captured CUDA graph (bench.py's timed path)."""
+    torch = _torch()
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    g = load_golden("bench")
+    nodes, x = _bench_config(arch)
+    gg = GpuGraph(nodes)
+    xd = torch.from_numpy(x).cuda()
+    trace = {}
+    y = gg.run(xd, trace=trace)
+    checked = 0
+    for cid, want in zip(g[f"{arch}_conv_ids"], g[f"{arch}_conv_sha"]):
+        plan = gg.conv_plans[str(cid)]
+        if plan.relu or plan.residual is not None:  # fused Add/ReLU: covered by the logits
+            continue
+        assert _sha(trace[str(cid)]) == want.tobytes(), cid
+        checked += 1
+    assert checked >= 1
+    del trace
+    assert _sha(y) == g[f"{arch}_logits_sha"].tobytes()
+    am = y.reshape(y.shape[0], -1).argmax(1).cpu().numpy()
+    assert np.array_equal(am, g[f"{arch}_argmax"])
+    gg.autotune(xd)
+    gg.capture(tuple(xd.shape))
+    y2 = gg.replay(xd)
+    assert _sha(y2) == g[f"{arch}_logits_sha"].tobytes()
+
+
+def test_r50_full_batch_grid_invariant():
+    """ResNet-50 at 256 images on a 100-SM persistent grid (other tile-to-CTA assignment) gives the
+    reference's bits (the grid size must never change results)."""
+    torch = _torch()
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    g = load_golden("bench")
+    nodes, x = _bench_config("r50")
+    y = GpuGraph(nodes, sm_limit=100).run(torch.from_numpy(x).cuda())
+    assert _sha(y) == g["r50_logits_sha"].tobytes()
 
 
 def test_exact_lut_control_full_size_layer():
@@ -532,8 +577,9 @@ def test_graph_on_cifar_records_matches_images():
 
 @pytest.mark.parametrize("mode", [O.SIGNED, O.UNSIGNED])
 def test_fused_quantize_im2col_equals_two_pass(mode):
-    """axb_quantize_im2col (one pass, fp32 -> code rows) == axb_quantize_pad + axb_im2col_pack,
-    rows and row sums, with host parameters and with in-kernel coefficients of a device range."""
+    """axb_quantize_im2col (one pass, fp32 -> code rows) == axb_quantize_pad + axb_im2col_pack ==
+    the oracle's im2cols (code rows + patch sums), with host parameters and with in-kernel
+    coefficients of a device range."""
     torch = _torch()
     from paper_2002_09481_b200 import _lib
 
@@ -586,6 +632,14 @@ def test_fused_quantize_im2col_equals_two_pass(mode):
             assert torch.equal(rows1, rows2), (n, h, w, c, kh, kw, use_range)
             assert torch.equal(sum1, sum2)
             assert int(fl[1].item()) == 0
+            # and both equal the oracle's im2cols (axconv.py:160-196): code rows (raw bytes, zero beyond K)
+            # and patch sums
+            sc, zp = O.compute_coeffs(float(x.min()), float(x.max()), mode)
+            mat, sums = O.im2cols(x, sc, zp, mode, O.HALF_AWAY, kh, kw, pads, (s, s), (d, d))
+            kk = kh * kw * c
+            got = rows2.cpu().numpy().reshape(-1, kp)
+            assert np.array_equal(got[:, :kk], mat.view(np.uint8)) and not got[:, kk:].any()
+            assert np.array_equal(sum2.cpu().numpy(), sums)
 
 
 def test_graph_autotune_keeps_bits():
@@ -604,6 +658,9 @@ def test_graph_autotune_keeps_bits():
     want = g.run(x).cpu().numpy()
     picks = g.autotune(x, reps=1)
     assert len(picks) == 10 and all(v.startswith(("ft", "cm")) or v == "lut_bmajor" for v in picks.values()), picks
+    # only the table layout each layer's pick reads stays resident
+    for p in g.conv_plans.values():
+        assert p.layer.ftable is None or p.layer.ftable_cm is None, p.node["id"]
     assert bits_equal(g.run(x).cpu().numpy(), want)
     g.set_tuning({nid: -1 for nid in g.tuning()})
     prof = []
@@ -705,7 +762,7 @@ def test_wide_channel_quantize_and_lut_kernel_pixsum(c):
 def test_pools_match_oracle(kind, c):
     """MaxPool / AvgPool (graph.py:182-199) through the executor vs the oracle, bit for bit: valid and
     explicit/same padding, strided and global windows, NaN and inf inputs (c % 4 == 0 takes the
-    vectorised kernel, c = 3 the scalar one)."""
+    vectorised kernel, c = 3 the scalar one), windows of -0.0 only."""
     torch = _torch()
     from paper_2002_09481_b200.graph import GpuGraph
 
@@ -714,6 +771,7 @@ def test_pools_match_oracle(kind, c):
     x[0, 1, 2, 0] = np.nan
     x[1, 4, 4, c - 1] = np.inf
     x[2, 8, 10, 0] = -np.inf
+    x[1, 0:3, 0:3, :] = -0.0  # an all -0.0 window: nansum starts from +0.0 (numpy), so AvgPool gives +0.0
     for attrs in ({"pool": [3, 3], "strides": [2, 2], "padding": "same"},
                   {"pool": [2, 2], "strides": [2, 2], "padding": "valid"},
                   {"pool": [3, 2], "strides": [1, 2], "padding": [1, 0, 1, 1]},
@@ -739,7 +797,10 @@ def test_ftable_kernel_long_k_packed_sums_exact(mode):
     case.update(in_range=(float(case["x"].min()), float(case["x"].max())),
                 f_range=(float(case["f"].min()), float(case["f"].max())))
     want, want_acc = oracle_conv(case, return_acc=True)
-    for v in range(1, _lib.load().axb_ft_variant_count()):
+    lib = _lib.load()
+    for v in range(1, lib.axb_ft_variant_count()):
+        if lib.axb_ft_variant_layout(v) == 2:  # 64-channel blocks: cout 20 pads to 32 (covered below)
+            continue
         y, acc, kern = gpu_conv(case, ft_variant=v)
         assert kern.startswith(("ft", "cm")), kern
         assert bits_equal(y, want), kern
@@ -810,22 +871,30 @@ def test_projection_reads_first_conv_codes():
     assert gg.launches == 1 + 10 + 10 - 2 + 1  # input range, 10 convs, 10 quantizes minus 2 shared, pool
 
 
+@pytest.mark.parametrize("layout", [1, 2])
 @pytest.mark.parametrize("mode", [O.SIGNED, O.UNSIGNED])
-def test_code_major_variants_vs_oracle(mode):
-    """The code-major kernel family (cm32_*: 32-channel blocks, LDS.128 of 4 pairs) over shapes the
-    pair-major test does not reach: cout 32 / 64 / 96 (one to three channel blocks, ragged 61), wide
-    and odd input channels, stride 2, dilation 2, ragged pixel tiles, every accumulator mode."""
+def test_code_major_variants_vs_oracle(mode, layout):
+    """The code-major kernel families -- cm32_* (32-channel blocks, LDS.128 of 4 pairs, layout 1) and
+    c64_* (64-channel blocks, one pixel per quarter-warp, layout 2) -- over shapes the pair-major test
+    does not reach: cout 32 / 64 / 96 / 128 / 192 (one to three channel blocks, ragged 61 and 150), wide
+    and odd input channels, stride 2, dilation 2, ragged pixel tiles, every accumulator mode, K = 4608."""
     from paper_2002_09481_b200 import _lib
 
     lib = _lib.load()
-    cms = [v for v in range(1, lib.axb_ft_variant_count()) if lib.axb_ft_variant_layout(v) == 1]
+    cms = [v for v in range(1, lib.axb_ft_variant_count()) if lib.axb_ft_variant_layout(v) == layout]
     assert len(cms) >= 3
+    blk = 32 if layout == 1 else 64
     rng = np.random.default_rng(4096 + (mode == O.SIGNED))
     shapes = [((3, 9, 13, 16), (3, 3, 16, 32), (1, 1), (1, 1), "same", O.EXACT64),
               ((2, 11, 10, 48), (3, 3, 48, 64), (2, 2), (1, 1), "same", O.WRAP32),
               ((2, 12, 12, 64), (1, 1, 64, 96), (1, 1), (1, 1), "valid", O.SATURATE32),
-              ((1, 14, 9, 37), (3, 3, 37, 61), (1, 2), (2, 2), "same", O.EXACT64)]
+              ((1, 14, 9, 37), (3, 3, 37, 61), (1, 2), (2, 2), "same", O.EXACT64),
+              ((3, 17, 15, 32), (3, 3, 32, 128), (1, 1), (1, 1), "same", O.EXACT64),
+              ((2, 9, 9, 80), (1, 1, 80, 150), (2, 2), (1, 1), "valid", O.WRAP32),
+              ((1, 5, 6, 512), (3, 3, 512, 192), (1, 1), (1, 1), "same", O.EXACT64)]
     for xs, fs, st, dil, pad, acc in shapes:
+        if -(-fs[3] // 16) * 16 % blk:
+            continue
         x = np.maximum(rng.standard_normal(xs), 0).astype(np.float32) if acc != O.WRAP32 else \
             rng.uniform(-2, 3, xs).astype(np.float32)
         case = dict(x=x, f=rng.standard_normal(fs).astype(np.float32), lut=O.random_lut(rng, mode), mode=mode,
@@ -835,7 +904,7 @@ def test_code_major_variants_vs_oracle(mode):
         want, want_acc = oracle_conv(case, return_acc=True)
         for v in cms:
             y, acc_got, kern = gpu_conv(case, ft_variant=v)
-            assert kern.startswith("cm32"), kern
+            assert kern.startswith("cm32" if layout == 1 else "c64"), kern
             assert bits_equal(y, want), (kern, xs, fs)
             assert np.array_equal(acc_got, want_acc), (kern, xs, fs)
 
@@ -855,10 +924,63 @@ def test_graph_forced_code_major_matches_reference():
     x = torch.from_numpy(g["r8_trunc2_x"]).cuda()
     gg.run(x)
     for v in [v for v in range(1, lib.axb_ft_variant_count()) if lib.axb_ft_variant_layout(v) == 1]:
-        picks = {nid: (v if p.layer.ftable_cm is not None else 0) for nid, p in gg.conv_plans.items()}
+        picks = {nid: (v if p.layer.cm_ok else 0) for nid, p in gg.conv_plans.items()}
         assert sum(1 for p in picks.values() if p) >= 5, picks
         gg.set_tuning(picks)
         prof = []
         y = gg.run(x, profile=prof).cpu().numpy()
         assert sum(1 for *_, fam in prof if fam == "lutconv_ftcm") == sum(1 for p in picks.values() if p)
         assert bits_equal(y, g["r8_trunc2_logits"]), lib.axb_ft_variant_name(v)
+
+
+def test_graph_rejects_range_nodes_over_another_tensor():
+    """An AxConv2D whose Min/Max inputs range over a different tensor than its data input (the reference
+    would quantize with that other range, graph.py:248-251) is refused at planning time instead of
+    silently quantizing with the data input's range slot."""
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    f = np.ones((1, 1, 3, 4), np.float32)
+    conv = {"filters": f, "strides": (1, 1), "dilations": (1, 1), "padding": "valid", "f_min": 0.0, "f_max": 1.0,
+            "lut": _lut(O.exact_lut(O.SIGNED), O.SIGNED)}
+    base = [{"id": "in", "kind": "Input", "inputs": [], "attrs": {}},
+            {"id": "r", "kind": "ReLU", "inputs": ["in"], "attrs": {}}]
+    bad = base + [{"id": "lo", "kind": "Min", "inputs": ["r"], "attrs": {}},
+                  {"id": "hi", "kind": "Max", "inputs": ["r"], "attrs": {}},
+                  {"id": "c", "kind": "AxConv2D", "inputs": ["in", "lo", "hi"], "attrs": conv}]
+    with pytest.raises(ValueError, match="range input"):
+        GpuGraph(bad)
+    swapped = base + [{"id": "lo", "kind": "Min", "inputs": ["in"], "attrs": {}},
+                      {"id": "hi", "kind": "Max", "inputs": ["in"], "attrs": {}},
+                      {"id": "c", "kind": "AxConv2D", "inputs": ["in", "hi", "lo"], "attrs": conv}]
+    with pytest.raises(ValueError, match="must be a Min node"):
+        GpuGraph(swapped)
+    good = base + [{"id": "lo", "kind": "Min", "inputs": ["in"], "attrs": {}},
+                   {"id": "hi", "kind": "Max", "inputs": ["in"], "attrs": {}},
+                   {"id": "c", "kind": "AxConv2D", "inputs": ["in", "lo", "hi"], "attrs": conv}]
+    GpuGraph(good)
+
+
+def test_graph_frees_intermediates_after_last_reader():
+    """Activations are released after their last executed reader (fused Add/ReLU and Min/Max nodes read
+    nothing at run time): ResNet-50 at 64 images peaks well below the sum of all its activations."""
+    torch = _torch()
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    nodes, x = _bench_config("r50")
+    gg = GpuGraph(nodes)
+    xd = torch.from_numpy(x[:64]).cuda()
+    gg.run(xd)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    trace = {}
+    gg.run(xd, trace=trace)  # trace keeps every node's value alive
+    torch.cuda.synchronize()
+    keep_all = torch.cuda.max_memory_allocated() - base
+    del trace
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    gg.run(xd)
+    torch.cuda.synchronize()
+    freed = torch.cuda.max_memory_allocated() - base
+    assert freed < 0.35 * keep_all, (freed, keep_all)

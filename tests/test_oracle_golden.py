@@ -133,3 +133,25 @@ def test_mac_counts():
     assert resnet.macs_per_image(resnet.resnet50(lut)) == 4_087_136_256 + 2_048_000
     nodes = oracle_nodes(resnet.cifar_resnet(1, lut))
     assert O.graph_mac_count(nodes, (3, 32, 32, 3)) == 3 * (12_500_992 + 640)
+
+
+@pytest.mark.parametrize("tag,classes", [("r8_trunc2", 5), ("r8_random", 5), ("r8_unsigned", 3), ("r62_trunc3", 3),
+                                         ("r50_exact", 3)])
+def test_golden_networks_are_not_degenerate(tag, classes):
+    """Calibrated networks (resnet.apply_calibration) predict different classes for different images, so
+    argmax parity means something: >= 5 distinct classes among 16 images; >= 3 for the 8-image and
+    4-image nets and for the 63-conv ResNet-62 under the 3-bit-truncating table (its calibration batch
+    has 1000 images; ranges are per batch, so 32 images shift every layer's quantization)."""
+    g = load_golden("nets")
+    am = g[f"{tag}_argmax"]
+    assert len(set(am.tolist())) >= classes, (tag, am)
+    rows = g[f"{tag}_logits"].reshape(len(am), -1)
+    assert len({r.tobytes() for r in rows}) == len(rows)  # no two images share a logits row
+
+
+def test_bench_goldens_are_not_degenerate():
+    """The benchmarked batches (ResNet-8 b1024, ResNet-50 b256): many classes predicted."""
+    g = load_golden("bench")
+    assert len(set(g["r8_argmax"].tolist())) >= 8
+    assert len(set(g["r50_argmax"].tolist())) >= 20
+    assert len(g["r8_conv_ids"]) == 10 and len(g["r50_conv_ids"]) == 54
