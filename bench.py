@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark: approximate-LUT ResNet inference on B200 (one process per GPU).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload r50|r8|r62|r62sweep]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload r50|r8|r62|r62sweep|mbv1]
                     [--impl b200|reference] [--stub]
 
 A step = one range-batch of synthetic images through the whole transformed
@@ -89,6 +89,10 @@ def workload_spec(name: str, lut_kind: str):
     if name == "r50":
         return dict(nodes=resnet.resnet50(lut, seed=0), batch=256, kind="imagenet", lut=lut_desc,
                     desc="ResNet-50 v1.5 224x224 (53 convs + 1x1 AxConv2D classifier), BN folded, calibrated")
+    if name == "mbv1":
+        return dict(nodes=resnet.mobilenet_v1(lut, seed=0), batch=256, kind="imagenet", lut=lut_desc,
+                    desc="MobileNet-v1-shaped 224x224 (stem + 13 x (depthwise 3x3 + pointwise 1x1) + 1x1 AxConv2D "
+                         "classifier; config 5 depthwise approximate conv), BN folded, calibrated")
     if name == "r62sweep":
         return dict(nodes=resnet.cifar_resnet(10, sweep_luts()[0], seed=0), batch=1000, kind="cifar",
                     lut="32 candidates: truncated_lut(mode, d) d=0..7 x {signed, unsigned} + 16 perturbed_lut "
@@ -647,7 +651,7 @@ def main(argv=None):
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="r50", choices=["r8", "r50", "r62", "r62sweep"])
+    ap.add_argument("--workload", default="r50", choices=["r8", "r50", "r62", "r62sweep", "mbv1"])
     ap.add_argument("--lut", default="trunc2", choices=["trunc2", "exact", "random"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])

@@ -367,6 +367,35 @@ def direct_conv(x, f, in_range, f_range, entries, mode, padding="valid", strides
     return ((s1 * s2) * corr).astype(np.float32)
 
 
+def depthwise_conv(x, f, in_range, f_range, entries, mode, padding="valid", strides=(1, 1),
+                   dilations=(1, 1), accumulator=EXACT64, round_mode=HALF_AWAY, return_acc=False):
+    """Depthwise approximate conv (BASELINE config 5; the reference has no grouped conv, tensor.py:66-87).
+
+    Defined as the per-channel decomposition SURVEY.md 8(d) config 5 prescribes: output channel c =
+    axconv2d(x[..., c:c+1], f[:, :, c:c+1, :]) (axconv.py:266-297) with the SAME input and filter
+    ranges for every channel.  f is (kh, kw, C, 1) (channel multiplier 1).
+    """
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    f = np.ascontiguousarray(f, dtype=np.float32)
+    if f.ndim != 4 or f.shape[3] != 1:
+        raise ValueError("depthwise filters must be (kh, kw, channels, 1)")
+    if x.shape[3] != f.shape[2]:
+        raise ValueError(f"filter channels {f.shape[2]} do not match input channels {x.shape[3]}")
+    parts = [axconv2d(x[..., c:c + 1], f[:, :, c:c + 1, :], in_range, f_range, entries, mode, padding=padding,
+                      strides=strides, dilations=dilations, accumulator=accumulator, round_mode=round_mode,
+                      return_acc=return_acc) for c in range(x.shape[3])]
+    if return_acc:
+        return (np.concatenate([o for o, _ in parts], axis=3), np.concatenate([a for _, a in parts], axis=3))
+    return np.concatenate(parts, axis=3)
+
+
+def conv_filter_shape(attrs) -> tuple:
+    """The dense-equivalent (kh, kw, cin, cout) of an AxConv2D node's filters: a depthwise node's
+    (kh, kw, C, 1) filters act as (kh, kw, 1, C) per channel -- MACs n*oh*ow*kh*kw*C."""
+    f = attrs["filters"]
+    return (f.shape[0], f.shape[1], 1, f.shape[2]) if attrs.get("depthwise") else tuple(f.shape)
+
+
 def conv_mac_count(in_shape, f_shape, padding, strides, dilations) -> int:
     """axconv.py:106-114"""
     n, oh, ow, cout = output_shape(in_shape, f_shape, padding, strides, dilations)
@@ -415,9 +444,10 @@ def run_graph(nodes, batch, accumulator=EXACT64, round_mode=HALF_AWAY, engine="g
     Kinds: Input, AxConv2D, Min, Max, ReLU, MaxPool, AvgPool, Add, Flatten,
     Dense, Softmax (the reference's names).  AxConv2D attrs: filters (HWCN),
     bias (optional), lut (entries), mode, f_min, f_max, strides, dilations,
-    padding.  engine "gemm" -> axconv2d, "direct" -> direct_conv.
+    padding, depthwise (optional: (kh, kw, C, 1) filters -> depthwise_conv, config 5).
+    engine "gemm" -> axconv2d, "direct" -> direct_conv.
     """
-    conv = axconv2d if engine == "gemm" else direct_conv
+    dense_conv = axconv2d if engine == "gemm" else direct_conv
     values = {}
     out = None
     for node in nodes:
@@ -430,6 +460,7 @@ def run_graph(nodes, batch, accumulator=EXACT64, round_mode=HALF_AWAY, engine="g
             padding = attrs.get("padding", "valid")
             if isinstance(padding, list):
                 padding = tuple(padding)
+            conv = depthwise_conv if attrs.get("depthwise") else dense_conv
             y = conv(ins[0], attrs["filters"], (float(ins[1]), float(ins[2])),
                      (attrs["f_min"], attrs["f_max"]), attrs["lut"], attrs["mode"],
                      padding=padding, strides=tuple(attrs.get("strides", (1, 1))),
@@ -491,8 +522,10 @@ def graph_mac_count(nodes, batch_shape) -> int:
                 padding = tuple(padding)
             st = tuple(attrs.get("strides", (1, 1)))
             dl = tuple(attrs.get("dilations", (1, 1)))
-            total += conv_mac_count(x, attrs["filters"].shape, padding, st, dl)
-            shapes[node["id"]] = output_shape(x, attrs["filters"].shape, padding, st, dl)
+            fs = conv_filter_shape(attrs)
+            xs = (x[0], x[1], x[2], 1) if attrs.get("depthwise") else x
+            total += conv_mac_count(xs, fs, padding, st, dl)
+            shapes[node["id"]] = output_shape(xs, fs, padding, st, dl)
         elif kind in ("Min", "Max"):
             shapes[node["id"]] = ()
         elif kind in ("ReLU", "Softmax", "Add"):

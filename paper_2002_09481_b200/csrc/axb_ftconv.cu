@@ -613,33 +613,43 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
 // data-dependent bank conflicts (the pair-major and 32-channel layouts lose 30-50% of their wavefronts to
 // conflicts on real activations).  Table bytes staged per product = 512 / BM (BM = WARPS * 4 * J pixels).
 // Registers: a lane holds 8 accumulator words per pixel (J pixels), so the activation codes do not live
-// in registers ahead of use: each warp stages its 32 pixels' next 16-row chunk in its own shared buffer
-// with cp.async (lane L copies pixel L's 16 bytes), lanes read 8 rows per pixel (LDS.64, broadcast over
-// the pixel's 8 lanes), and lane L sums pixel L's codes (S_p, DP4A) -- shuffled to its lanes at the end.
+// in registers ahead of use: each warp stages its PXW = 4*J pixels' next 16-row chunk in its own shared
+// buffer with cp.async (lane L copies pixels L, L+32, ...: 16 bytes each), lanes read CR rows per pixel
+// (LDS.64 for CR = 8, LDS.32 for CR = 4 -- half the code registers), and lane L sums its staged pixels'
+// codes (S_p, DP4A) -- shuffled to the pixel's lanes at the end.
+// Why J = 16: the table stages are the kernel's L2 traffic, 512 / BM bytes per product (32 KiB per row
+// and 64-channel block, read once per BM-pixel tile).  With BM = 384 (J = 8, 12 warps) that is 1.33 B per
+// product -- at ~8.8e12 products/s, 11 TB/s of L2->SM traffic, the chip's L2 read ceiling -- so the tile
+// has to grow: J = 16 at 8 or 10 warps (BM = 512 / 640) cuts it to 1.0 / 0.8 B per product.
 constexpr int kC64Pairs = 32;                   // channel pairs per 64-channel block
 constexpr int kC64RowWords = 256 * kC64Pairs;   // one (block, row) slice: 256 codes x 32 pairs
 constexpr int kC64RowBytes = kC64RowWords * 4;  // 32 KiB
 __host__ __device__ constexpr int c64_stage_bytes(int KS) { return KS * kC64RowBytes; }
-__host__ __device__ constexpr int c64_codebuf_bytes(int WARPS) { return WARPS * 2 * 32 * 16; }
-__host__ __device__ constexpr int c64_smem(int KS, int ST, int WARPS) {
-    return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS) + kMaxTaps * 4 + 2 * ST * 8;
+__host__ __device__ constexpr int c64_codebuf_bytes(int WARPS, int J) { return WARPS * 2 * 4 * J * 16; }
+__host__ __device__ constexpr int c64_smem(int KS, int ST, int WARPS, int J) {
+    return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS, J) + kMaxTaps * 4 + 2 * ST * 8;
 }
 
-template <int J, int WARPS, int KS, int ST, bool SGN>
+template <int J, int WARPS, int KS, int ST, bool SGN, int CR>
 __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     constexpr int NT = WARPS * 32;
     constexpr int PXW = 4 * J;        // pixels per warp
+    constexpr int NPL = PXW / 32;     // pixels whose codes each lane stages
     constexpr int BM = WARPS * PXW;
     constexpr int BN = 64;
-    constexpr int SPH = 8 / KS;       // stages per 8-row half chunk
+    constexpr int SPG = CR / KS;      // stages per CR-row code group
+    constexpr int NG = 16 / CR;       // code groups per 16-row chunk
+    constexpr int CBW = PXW * 16;     // one of a warp's two code buffers (bytes)
     constexpr uint32_t STAGE_BYTES = c64_stage_bytes(KS);
-    static_assert(PXW == 32, "one staged code row per lane: 32 pixels per warp (J = 8)");
+    static_assert(PXW % 32 == 0, "whole 32-pixel groups per warp (J = 8 or 16)");
+    static_assert(CR == 4 || CR == 8, "code rows per register load: 4 (LDS.32) or 8 (LDS.64)");
     static_assert(KS == 1 || KS == 2 || KS == 4, "KS rows per stage: 1, 2 or 4");
-    static_assert(c64_smem(KS, ST, WARPS) + 512 <= 232448, "C64 ring exceeds shared memory");
+    static_assert(CR % KS == 0, "a stage never straddles two code groups");
+    static_assert(c64_smem(KS, ST, WARPS, J) + 512 <= 232448, "C64 ring exceeds shared memory");
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *codebuf = smem + ST * STAGE_BYTES;  // [warp][2][32 pixels][16 B]
-    int32_t *tapoff_s = reinterpret_cast<int32_t *>(codebuf + c64_codebuf_bytes(WARPS));
+    uint8_t *codebuf = smem + ST * STAGE_BYTES;  // [warp][2][PXW pixels][16 B]
+    int32_t *tapoff_s = reinterpret_cast<int32_t *>(codebuf + c64_codebuf_bytes(WARPS, J));
     uint64_t *full = reinterpret_cast<uint64_t *>(tapoff_s + kMaxTaps);
     uint64_t *empty = full + ST;
 
@@ -662,7 +672,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     const int grid = (int)gridDim.x;
     const int cid = (int)blockIdx.x;
     const int my_tiles = p.ntiles > cid ? (int)((p.ntiles - cid + grid - 1) / grid) : 0;
-    const int spt = p.nchunks * 2 * SPH;  // stages per tile
+    const int spt = p.nchunks * (16 / KS);  // stages per tile
     const int total = my_tiles * spt;
 
     int pr_h = 0, pr_q = 0, pr_tile = cid, pr_slot = 0;
@@ -681,21 +691,27 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     if (tid == 0)
         for (int s = 0; s < ST - 1 && pr_h < total; ++s) produce();
 
-    // ---- code loader: lane L stages pixel L (of this warp's 32) one 16-row chunk ahead
-    uint8_t *wbuf = codebuf + warp * (2 * 32 * 16);
-    int32_t rowbase = 0;  // byte offset of lane L's pixel in the zp-padded code tensor
+    // ---- code loader: lane L stages pixels L, L+32, ... (of this warp's PXW) one 16-row chunk ahead
+    uint8_t *wbuf = codebuf + warp * (2 * CBW);
+    int32_t rowbase[NPL];  // byte offset of each staged pixel in the zp-padded code tensor
     auto set_row = [&](int tile) {
-        const int64_t mt = (int64_t)(tile % p.ntm) * BM + warp * PXW + lane;
-        int64_t pix0 = 0;
-        if (mt < p.M) pixel_of(p, mt, pix0);
-        rowbase = (int32_t)(pix0 * p.cs);
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) {
+            const int64_t mt = (int64_t)(tile % p.ntm) * BM + warp * PXW + lane + 32 * i;
+            int64_t pix0 = 0;
+            if (mt < p.M) pixel_of(p, mt, pix0);
+            rowbase[i] = (int32_t)(pix0 * p.cs);
+        }
     };
     pdl_wait();
     int ld_t = 0, ld_ci = 0, ld_kc = 0, ld_buf = 0;
     int ld_left = my_tiles * p.nchunks, ld_tile = cid;
     auto load_next = [&]() {
         if (ld_left > 0) {
-            cp_async16(wbuf + ld_buf * 512 + lane * 16, p.codes + rowbase + tapoff_s[ld_t] + ld_ci, 16);
+            const int off = tapoff_s[ld_t] + ld_ci;
+#pragma unroll
+            for (int i = 0; i < NPL; ++i)
+                cp_async16(wbuf + ld_buf * CBW + (lane + 32 * i) * 16, p.codes + rowbase[i] + off, 16);
             --ld_left;
             ld_ci += 16;
             if (ld_ci == p.cs) {
@@ -717,7 +733,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     for (int j = 0; j < J; ++j)
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc_all[j][r] = acc_hi[j][r] = 0;
-    int32_t spl = 0;  // S_p of lane L's pixel
+    int32_t spl[NPL];  // S_p of lane L's staged pixels
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) spl[i] = 0;
     float tmin = INFINITY, tmax = -INFINITY;
     int nonfinite = 0;
     const int64_t bias_units = SGN ? (int64_t)32768 * p.kpad : 0;
@@ -737,29 +755,39 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
             __syncwarp();   // every lane is done reading the buffer the next copy overwrites
             load_next();    // chunk kc+1 -> the other buffer
             cp_async_wait<1>();
-            __syncwarp();   // chunk kc of all 32 pixels has landed
-            const uint8_t *cb_ = wbuf + cbuf * 512;
-            {  // S_p of pixel L (axconv.py:193; junk codes are raw 0 -> value 0)
-                const uint4 mine = *reinterpret_cast<const uint4 *>(cb_ + lane * 16);
+            __syncwarp();   // chunk kc of all PXW pixels has landed
+            const uint8_t *cb_ = wbuf + cbuf * CBW;
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) {  // S_p of the staged pixels (axconv.py:193; junk codes are raw 0)
+                const uint4 mine = *reinterpret_cast<const uint4 *>(cb_ + (lane + 32 * i) * 16);
                 if (SGN) {
-                    spl = __dp4a((int)mine.x, 0x01010101, spl);
-                    spl = __dp4a((int)mine.y, 0x01010101, spl);
-                    spl = __dp4a((int)mine.z, 0x01010101, spl);
-                    spl = __dp4a((int)mine.w, 0x01010101, spl);
+                    spl[i] = __dp4a((int)mine.x, 0x01010101, spl[i]);
+                    spl[i] = __dp4a((int)mine.y, 0x01010101, spl[i]);
+                    spl[i] = __dp4a((int)mine.z, 0x01010101, spl[i]);
+                    spl[i] = __dp4a((int)mine.w, 0x01010101, spl[i]);
                 } else {
-                    uint32_t t = __dp4a(mine.x, 0x01010101u, (uint32_t)spl);
+                    uint32_t t = __dp4a(mine.x, 0x01010101u, (uint32_t)spl[i]);
                     t = __dp4a(mine.y, 0x01010101u, t);
                     t = __dp4a(mine.z, 0x01010101u, t);
-                    spl = (int32_t)__dp4a(mine.w, 0x01010101u, t);
+                    spl[i] = (int32_t)__dp4a(mine.w, 0x01010101u, t);
                 }
             }
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                uint2 cur[J];
+            for (int gr = 0; gr < NG; ++gr) {
+                uint32_t cur[J][CR / 4];
 #pragma unroll
-                for (int j = 0; j < J; ++j) cur[j] = *reinterpret_cast<const uint2 *>(cb_ + (j * 4 + ps) * 16 + hh * 8);
+                for (int j = 0; j < J; ++j) {
+                    const uint8_t *src = cb_ + (j * 4 + ps) * 16 + gr * CR;
+                    if (CR == 8) {
+                        const uint2 v = *reinterpret_cast<const uint2 *>(src);
+                        cur[j][0] = v.x;
+                        cur[j][CR / 4 - 1] = v.y;
+                    } else {
+                        cur[j][0] = *reinterpret_cast<const uint32_t *>(src);
+                    }
+                }
 #pragma unroll
-                for (int st = 0; st < SPH; ++st) {
+                for (int st = 0; st < SPG; ++st) {
                     if (tid == 0 && pr_h < total) {
                         // refill the slot stage g-1 used once every warp released it
                         if (g >= 1) {
@@ -773,10 +801,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
                     const uint8_t *stab = tab_lane + slot * STAGE_BYTES;
 #pragma unroll
                     for (int kl = 0; kl < KS; ++kl) {
-                        const int r = st * KS + kl;  // row within the half chunk (compile-time)
+                        const int r = st * KS + kl;  // row within the code group (compile-time)
 #pragma unroll
                         for (int j = 0; j < J; ++j) {
-                            const uint32_t a = __byte_perm(r < 4 ? cur[j].x : cur[j].y, 0, 0x4440u + (r & 3));
+                            const uint32_t a = __byte_perm(cur[j][r >> 2], 0, 0x4440u + (r & 3));
                             const uint4 w = *reinterpret_cast<const uint4 *>(stab + kl * kC64RowBytes + a * 128u);
                             acc_all[j][0] += w.x; acc_hi[j][0] += w.x >> 16;
                             acc_all[j][1] += w.y; acc_hi[j][1] += w.y >> 16;
@@ -806,7 +834,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
             const bool full_blk = cb + 8 <= p.cout && (p.cout & 3) == 0;
 #pragma unroll
             for (int j = 0; j < J; ++j) {
-                const int32_t spj = __shfl_sync(0xffffffffu, spl, j * 4 + ps);
+                const int32_t spj = __shfl_sync(0xffffffffu, spl[j >> 3], (j * 4 + ps) & 31);
                 const int64_t mt = m0 + warp * PXW + j * 4 + ps;
                 if (mt < p.M) {
                     int64_t pix0;
@@ -868,7 +896,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) acc_all[j][r] = acc_hi[j][r] = 0;
             }
-            spl = 0;
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) spl[i] = 0;
         }
         c_tile += grid;
     }
@@ -983,6 +1012,7 @@ static const FtVariant kFtVariants[] = {
     {"c64_j8_w12_k2", 8, 12, 32, 1, 1.000f, 2},
     {"c64_j8_w8_k2", 8, 8, 32, 1, 1.000f, 2},
     {"c64_j8_w16_k1", 8, 16, 32, 1, 1.000f, 2},
+    {"c64_j16_w8_k2", 16, 8, 32, 1, 1.000f, 2},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
@@ -1023,12 +1053,12 @@ static int launch_ftcm(int op, const ConvK &k, int sm_limit, cudaStream_t s, con
     return check_launch("lutconv_ftcm");
 }
 
-template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3>
+template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3, int CR = 8>
 static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WARPS * 4 * J;
     constexpr int BN = 64;
-    const size_t smem = c64_smem(KS, ST, WARPS);
-    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN>;
+    const size_t smem = c64_smem(KS, ST, WARPS, J);
+    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN, CR>;
     static int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1137,6 +1167,7 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 16: return launch_ftc64<8, 12, SGN>(op, k, sm_limit, s, nm);
         case 17: return launch_ftc64<8, 8, SGN>(op, k, sm_limit, s, nm);
         case 18: return launch_ftc64<8, 16, SGN, 1, 6>(op, k, sm_limit, s, nm);
+        case 19: return launch_ftc64<16, 8, SGN, 2, 3, 8>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }

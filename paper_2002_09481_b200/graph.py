@@ -231,13 +231,19 @@ class GpuGraph:
                 p = st.plan
                 xs = shapes[self.t(p.x)]
                 f = a["filters"]
+                dw = bool(a.get("depthwise", False))
                 p.geometry = _geometry(a)
                 p.in_shape = xs
-                p.out_shape = output_shape(xs, f.shape, p.geometry)
+                if dw:  # (kh, kw, C, 1) depthwise filters (config 5): output channels = input channels
+                    if f.ndim != 4 or f.shape[3] != 1 or f.shape[2] != xs[3]:
+                        raise ValueError(f"depthwise AxConv2D {n['id']!r}: filters must be (kh, kw, {xs[3]}, 1)")
+                    p.out_shape = output_shape(xs, (f.shape[0], f.shape[1], xs[3], xs[3]), p.geometry)
+                else:
+                    p.out_shape = output_shape(xs, f.shape, p.geometry)
                 shapes[n["id"]] = p.out_shape
                 if p.layer is None:
                     p.layer = ConvLayer(f, (a["f_min"], a["f_max"]), a["lut"], p.geometry, a.get("bias"),
-                                        self.round_name, self.acc_name, self.device.index)
+                                        self.round_name, self.acc_name, self.device.index, depthwise=dw)
             elif st.kind in ("ReLU", "Add"):
                 shapes[n["id"]] = shapes[self.t(n["inputs"][0])]
             elif st.kind in ("MaxPool", "AvgPool"):

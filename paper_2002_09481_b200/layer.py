@@ -253,8 +253,9 @@ class ConvLayer:
         else:
             codes = torch.empty(n * hp_ * wp_ * in_cs, dtype=torch.uint8, device=self.device)
             # the ftable kernel sums patch codes in its loop; only the LUT / generic kernels read pixsum
+            # (the depthwise kernel sums its own per-channel patch codes)
             ft = self.has_ft and use_ftable and not variant and not force_generic
-            pixsum = None if ft else torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
+            pixsum = None if ft or self.depthwise else torch.empty(n * hp_ * wp_, dtype=torch.int32, device=self.device)
             pix_ptr = pixsum.data_ptr() if pixsum is not None else None
             qbytes = x.numel() * 4 + codes.numel() + (pixsum.numel() * 4 if pixsum is not None else 0)
             if in_range_dev is not None:  # coefficients of the device range computed inside the quantize kernel
@@ -310,13 +311,13 @@ class ConvLayer:
         self.launches += 1
         if profile is not None:
             e1.record()
-            # algorithmic HBM bytes of the conv launch: codes (+ per-pixel sums), filter codes,
-            # fp32 output, residual read
             # algorithmic HBM bytes of the conv launch: codes (+ per-pixel sums), filter codes or the
             # filter-specialised product table (read once), fp32 output, residual read
             ft = d.ftable is not None
-            algo = d.n * d.hp * d.wp * (d.cs + 4) + (table.numel() * 4 if ft else self.kpad * self.coutp) \
+            algo = d.n * d.hp * d.wp * (d.cs + (4 if d.pixsum else 0)) \
+                + (table.numel() * 4 if ft else self.kpad * self.coutp) \
                 + n * oh * ow * self.cout * (8 if residual is not None else 4)
-            profile.append((e0, e1, n * oh * ow * self.kh * self.kw * c * self.cout, algo,
+            macs = n * oh * ow * self.kh * self.kw * (1 if self.depthwise else c) * self.cout
+            profile.append((e0, e1, macs, algo,
                             _lib.kernel_family(_lib.last_kernel())))
         return out

@@ -57,6 +57,18 @@ class _Builder:
             return self.add(f"{nid}.relu", "ReLU", [nid])
         return nid
 
+    def dwconv(self, nid, x, c, k, stride=1, relu=True):
+        """Depthwise k x k conv (channel multiplier 1): filters (k, k, c, 1), ``depthwise=True``."""
+        std = float(np.sqrt(2.0 / (k * k)))
+        f = (self.rng.standard_normal((k, k, c, 1)) * std).astype(np.float32)
+        b = (self.rng.standard_normal(c) * 0.05).astype(np.float32)
+        self.add(f"{nid}.in_min", "Min", [x])
+        self.add(f"{nid}.in_max", "Max", [x])
+        self.add(nid, "AxConv2D", [x, f"{nid}.in_min", f"{nid}.in_max"], filters=f, strides=(stride, stride),
+                 dilations=(1, 1), padding="same", lut=self.lut, f_min=float(f.min()), f_max=float(f.max()),
+                 bias=b, depthwise=True)
+        return self.add(f"{nid}.relu", "ReLU", [nid]) if relu else nid
+
 
 # ---------------------------------------------------------------------------- calibration
 
@@ -96,8 +108,8 @@ def calibration_key(arch_seed: str, lut) -> str:
 def apply_calibration(nodes, key: str) -> list[dict]:
     """Fold the committed calibration ``key`` (``scripts/make_calibration.py``) into the convs, in place.
 
-    Per conv: filters *= 2^exp (exact in fp32), bias = the calibrated per-channel bias; f_min / f_max
-    follow the filters (transform folds the filter range to constants, graph.py:129-130).
+    Per conv: filters *= 2^exp (exact in fp32; exp per layer, or per output channel), bias = the
+    calibrated per-channel bias; f_min / f_max follow the filters (transform folds the filter range to constants, graph.py:129-130).
     """
     cal = _calib()
     for nd in nodes:
@@ -108,7 +120,13 @@ def apply_calibration(nodes, key: str) -> list[dict]:
             raise KeyError(f"no calibration {key!r} for conv {nd['id']!r} (scripts/make_calibration.py); "
                            "build the network with calibrated=False")
         a = nd["attrs"]
-        f = (a["filters"] * np.float32(2.0 ** int(cal[ek]))).astype(np.float32)
+        e = np.asarray(cal[ek])
+        if e.ndim == 0:  # one power of two per layer: codes unchanged, output scaled exactly
+            f = (a["filters"] * np.float32(2.0 ** int(e))).astype(np.float32)
+        else:  # one per output channel (axis 3; axis 2 of (kh, kw, C, 1) depthwise filters)
+            sc = (2.0 ** e.astype(np.float64)).astype(np.float32)
+            f = (a["filters"] * (sc[None, None, :, None] if a.get("depthwise") else sc[None, None, None, :]))
+            f = f.astype(np.float32)
         a["filters"], a["bias"] = f, cal[bk].astype(np.float32)
         a["f_min"], a["f_max"] = float(f.min()), float(f.max())
     return nodes
@@ -167,6 +185,33 @@ def resnet50(lut, seed: int = 0, classes: int = 1000, calibrated: bool = True) -
     return g.nodes
 
 
+# MobileNet v1 (Howard et al. 2017, width 1.0): (stride, output channels) of the 13 depthwise-separable blocks
+MOBILENET_V1 = ((1, 64), (2, 128), (1, 128), (2, 256), (1, 256), (2, 512), (1, 512), (1, 512), (1, 512),
+                (1, 512), (1, 512), (2, 1024), (1, 1024))
+
+
+def mobilenet_v1(lut, seed: int = 0, classes: int = 1000, calibrated: bool = True) -> list[dict]:
+    """MobileNet-v1-shaped network (BASELINE config 5's depthwise approximate conv, in context): 224x224x3,
+    3x3/2 stem to 32 channels, 13 blocks of depthwise 3x3 (``depthwise=True``) + pointwise 1x1, global
+    average pool, 1x1 AxConv2D classifier; BN folded into every conv.  The depthwise layers include the
+    (n,112,112,32) and (n,56,56,128) shapes at stride 1 and 2 (blocks 0-3).  The reference has no
+    grouped conv: a depthwise node means per-channel ``axconv2d`` with shared ranges (oracle
+    ``depthwise_conv``)."""
+    g = _Builder(seed, lut)
+    g.add("in", "Input", shape=(224, 224, 3))
+    x = g.conv("stem", "in", 3, 32, 3, 2, relu=True)
+    c = 32
+    for i, (stride, cout) in enumerate(MOBILENET_V1):
+        x = g.dwconv(f"b{i}.dw", x, c, 3, stride)
+        x = g.conv(f"b{i}.pw", x, c, cout, 1, 1, relu=True)
+        c = cout
+    g.add("pool", "AvgPool", [x], pool=(7, 7), strides=(7, 7))
+    g.conv("fc", "pool", c, classes, 1)
+    if calibrated:
+        apply_calibration(g.nodes, calibration_key(f"mbv1_s{seed}", lut))
+    return g.nodes
+
+
 def single_conv(lut, seed: int = 0, in_shape=(32, 32, 3), cout: int = 16, k: int = 3) -> list[dict]:
     """Config 1: one approximate conv layer (3x3x3 -> 16, "same")."""
     g = _Builder(seed, lut)
@@ -197,8 +242,12 @@ def macs_per_image(nodes) -> int:
         elif k == "AxConv2D":
             x = shapes[nd["inputs"][0]]
             geo = ConvGeometry(tuple(a["strides"]), tuple(a["dilations"]), a["padding"])
-            o = output_shape(x, a["filters"].shape, geo)
-            kh, kw, cin, cout = a["filters"].shape
+            fs = a["filters"].shape
+            if a.get("depthwise"):  # (kh, kw, C, 1): C independent single-channel convs
+                fs = (fs[0], fs[1], 1, fs[2])
+                x = x[:3] + (1,)
+            o = output_shape(x, fs, geo)
+            kh, kw, cin, cout = fs
             total += o[1] * o[2] * kh * kw * cin * cout
             shapes[nd["id"]] = o
         elif k in ("Min", "Max"):

@@ -242,11 +242,43 @@ def make_nets() -> dict:
     return out
 
 
+class _DepthwiseDispatch:
+    """The reference has no grouped conv (tensor.py:66-87).  For graphs with depthwise AxConv2D nodes
+    (config 5) ``graph.run``'s conv (graph.py:226, :259-267) is wrapped: a node whose filters array is
+    registered here runs as per-channel reference ``axconv2d`` calls with the node's shared ranges
+    (SURVEY.md 8(d) config 5); every other conv runs the reference's ``axconv2d`` unchanged."""
+
+    def __init__(self, nodes):
+        import axemu.graph as G
+
+        self.G, self.orig = G, G.axconv2d
+        self.dw = {id(n["attrs"]["filters"]) for n in nodes if n["attrs"].get("depthwise")}
+
+    def __call__(self, inputs, filters, in_range, f_range, lut, cfg, meter=None):
+        if id(filters.data) not in self.dw:
+            return self.orig(inputs, filters, in_range, f_range, lut, cfg, meter)
+        x, f = inputs.data, filters.data
+        parts = [self.orig(Tensor4(x[..., c:c + 1], Layout.NHWC), Tensor4(f[:, :, c:c + 1, :], Layout.HWCN),
+                           in_range, f_range, lut, cfg, meter).data for c in range(x.shape[3])]
+        return Tensor4(np.concatenate(parts, axis=3), Layout.NHWC)
+
+    def __enter__(self):
+        self.G.axconv2d = self
+        return self
+
+    def __exit__(self, *exc):
+        self.G.axconv2d = self.orig
+
+
 def run_reference(tag, nodes, x, out):
     """Logits, argmax and per-conv output sha256 of ``nodes`` on ``x`` through the reference graph.run."""
+    for n in nodes:  # the filters object graph.run hands to the conv must stay the node's own array
+        if "filters" in n["attrs"]:
+            n["attrs"]["filters"] = np.ascontiguousarray(n["attrs"]["filters"], np.float32)
     g = to_reference_graph(nodes)
     trace = {}
-    y = axemu.run(g, Tensor4(x, Layout.NHWC), "gemm", trace=trace).data
+    with _DepthwiseDispatch(nodes):
+        y = axemu.run(g, Tensor4(x, Layout.NHWC), "gemm", trace=trace).data
     n = x.shape[0]
     out[f"{tag}_logits"] = y
     out[f"{tag}_argmax"] = y.reshape(n, -1).argmax(1)
@@ -272,7 +304,7 @@ def make_bench() -> dict:
 
     lut = T.truncated_lut(T.Signedness.SIGNED, 2)
     out = {}
-    which = [a for a in sys.argv[1:] if a in ("r8", "r50")] or ["r8", "r50"]
+    which = [a for a in sys.argv[1:] if a in ("r8", "r50", "mbv1")] or ["r8", "r50", "mbv1"]
     path = HERE / "bench.npz"
     if path.exists():
         out.update(dict(np.load(path)))
@@ -282,6 +314,9 @@ def make_bench() -> dict:
     if "r50" in which:
         x, _ = datasets.synthetic_imagenet(256, seed=BENCH_SEED)
         run_reference("r50", resnet.resnet50(lut, seed=0), x, out)
+    if "mbv1" in which:
+        x, _ = datasets.synthetic_imagenet(256, seed=BENCH_SEED)
+        run_reference("mbv1", resnet.mobilenet_v1(lut, seed=0), x, out)
     return out
 
 

@@ -344,6 +344,8 @@ def _bench_config(arch):
     lut = T.truncated_lut(T.Signedness.SIGNED, 2)
     if arch == "r8":  # BASELINE config 2, bench.py --workload r8, rank 0's batch
         return resnet.cifar_resnet(1, lut, seed=0), datasets.synthetic_cifar10(1024, seed=1000)[0]
+    if arch == "mbv1":  # config 5's depthwise conv in a MobileNet-v1-shaped net, bench.py --workload mbv1
+        return resnet.mobilenet_v1(lut, seed=0), datasets.synthetic_imagenet(256, seed=1000)[0]
     return resnet.resnet50(lut, seed=0), datasets.synthetic_imagenet(256, seed=1000)[0]  # config 3 (default)
 
 
@@ -351,9 +353,10 @@ def _sha(t) -> bytes:
     return hashlib.sha256(np.ascontiguousarray(t.cpu().numpy()).tobytes()).digest()
 
 
-@pytest.mark.parametrize("arch", ["r8", "r50"])
+@pytest.mark.parametrize("arch", ["r8", "r50", "mbv1"])
 def test_benchmarked_configs_bit_exact_vs_reference(arch):
-    """The benchmarked networks at their full batch -- ResNet-8 b1024 and ResNet-50 224x224 b256 with
+    """The benchmarked networks at their full batch -- ResNet-8 b1024, ResNet-50 224x224 b256 and the
+    MobileNet-v1-shaped net b256 (13 depthwise layers: per-channel reference axconv2d) with
     truncated_lut(signed, 2), calibrated weights -- against the REAL reference graph.run on the same
     batch (tests/golden/bench.npz): every unfused conv output, all logits, argmax.  Then again after the
     per-layer autotune, through the captured CUDA graph (bench.py's timed path)."""

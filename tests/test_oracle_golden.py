@@ -150,8 +150,51 @@ def test_golden_networks_are_not_degenerate(tag, classes):
 
 
 def test_bench_goldens_are_not_degenerate():
-    """The benchmarked batches (ResNet-8 b1024, ResNet-50 b256): many classes predicted."""
+    """The benchmarked batches (ResNet-8 b1024, ResNet-50 b256, MobileNet-v1-shaped b256): several classes
+    predicted (the 27-conv MobileNet with 9-tap depthwise layers is the least diverse)."""
     g = load_golden("bench")
     assert len(set(g["r8_argmax"].tolist())) >= 8
     assert len(set(g["r50_argmax"].tolist())) >= 20
-    assert len(g["r8_conv_ids"]) == 10 and len(g["r50_conv_ids"]) == 54
+    assert len(set(g["mbv1_argmax"].tolist())) >= 4
+    assert len(g["r8_conv_ids"]) == 10 and len(g["r50_conv_ids"]) == 54 and len(g["mbv1_conv_ids"]) == 28
+
+
+def test_depthwise_oracle_is_per_channel_axconv2d():
+    """Config 5's depthwise conv in the oracle graph: a node with depthwise=True and (kh, kw, C, 1) filters
+    equals the per-channel reference decomposition (axconv2d per channel, shared ranges); both engines."""
+    rng = np.random.default_rng(55)
+    x = np.maximum(rng.standard_normal((2, 9, 11, 5)), 0).astype(np.float32)
+    f = (rng.standard_normal((3, 3, 5, 1)) * 0.4).astype(np.float32)
+    lut = O.random_lut(rng, O.SIGNED)
+    nodes = [{"id": "in", "kind": "Input", "inputs": [], "attrs": {}},
+             {"id": "d.in_min", "kind": "Min", "inputs": ["in"], "attrs": {}},
+             {"id": "d.in_max", "kind": "Max", "inputs": ["in"], "attrs": {}},
+             {"id": "d", "kind": "AxConv2D", "inputs": ["in", "d.in_min", "d.in_max"],
+              "attrs": dict(filters=f, lut=lut, mode=O.SIGNED, f_min=float(f.min()), f_max=float(f.max()),
+                            strides=(2, 1), dilations=(1, 1), padding="same", depthwise=True)}]
+    ir, fr = (float(x.min()), float(x.max())), (float(f.min()), float(f.max()))
+    want = np.concatenate([O.axconv2d(x[..., c:c + 1], f[:, :, c:c + 1, :], ir, fr, lut, O.SIGNED, padding="same",
+                                      strides=(2, 1)) for c in range(5)], axis=3)
+    for engine in ("gemm", "direct"):
+        assert bits_equal(O.run_graph(nodes, x, engine=engine), want)
+    assert O.graph_mac_count(nodes, x.shape) == 2 * 5 * 11 * 9 * 5
+    with pytest.raises(ValueError, match="depthwise filters"):
+        O.depthwise_conv(x, np.zeros((3, 3, 5, 2), np.float32), ir, fr, lut, O.SIGNED)
+
+
+def test_mobilenet_shapes_and_macs():
+    """The MobileNet-v1-shaped net (config 5 in context): 13 depthwise + 14 dense convs, 568.7 M MACs per
+    image (the architecture's published 569 M mult-adds), depthwise layers at (112,112,32) and (56,56,128)
+    at stride 1 and 2, calibrated per output channel."""
+    from paper_2002_09481_b200 import resnet
+    from paper_2002_09481_b200 import types as T
+
+    nodes = resnet.mobilenet_v1(T.truncated_lut(T.Signedness.SIGNED, 2))
+    convs = [n for n in nodes if n["kind"] == "AxConv2D"]
+    dws = [n for n in convs if n["attrs"].get("depthwise")]
+    assert len(convs) == 28 and len(dws) == 13
+    assert resnet.macs_per_image(nodes) == 568_740_352
+    assert O.graph_mac_count(oracle_nodes(nodes), (1, 224, 224, 3)) == 568_740_352
+    shapes = [(n["attrs"]["filters"].shape, n["attrs"]["strides"]) for n in dws[:4]]
+    assert shapes == [((3, 3, 32, 1), (1, 1)), ((3, 3, 64, 1), (2, 2)), ((3, 3, 128, 1), (1, 1)),
+                      ((3, 3, 128, 1), (2, 2))]

@@ -44,6 +44,7 @@ def patched_graph():
     mod = types.ModuleType("axemu.graph_b200")
     mod.__package__ = "axemu"
     mod.__file__ = str(REF / "axemu" / "graph_b200.py")
+    sys.modules[mod.__name__] = mod  # dataclasses resolve annotations through sys.modules
     exec(compile(src, mod.__file__, "exec"), mod.__dict__)
     return mod
 
