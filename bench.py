@@ -603,7 +603,9 @@ def hbm_block(args, res, peak_gbs):
     """GB/s of the memory-bound kernels (range, record decode, quantize, pools, add) from the eager
     pass: algorithmic bytes (4 B per fp32 element read / written, 1 B per code) / event-timed launch."""
     agg: dict = {}
-    for _, kind, a, b, nbytes in res["extra"]["mprofile"]:
+    # the depthwise conv does 9 lookups per output: it is memory-bound too (codes in, fp32 out)
+    dw = [(nid, k, a, b, ab) for nid, a, b, _, ab, k in res["extra"]["profile"] if k.startswith("depthwise")]
+    for _, kind, a, b, nbytes in list(res["extra"]["mprofile"]) + dw:
         r = agg.setdefault(kind, [0, 0.0, 0])
         r[0] += 1
         r[1] += a.elapsed_time(b)

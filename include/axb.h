@@ -200,6 +200,14 @@ int axb_conv_variant_count(void);
  * desc: cout == c; fcodes/fsum from axb_filters_prepare on the (kh,kw,1,c)
  * view of the (kh,kw,c,1) filter (cs 16). */
 int axb_depthwise_lut(const axb_conv_desc *desc, const axb_lut *lut, void *stream);
+/* Channel-bank product table for the depthwise kernel (desc->ftable; <= 13 taps):
+ *   DW[cb][t][a >> 1][lane] = u(lut[(a_even << 8) | b]) | u(lut[(a_odd << 8) | b]) << 16
+ * b = filter code of tap t, channel cb*32 + lane; u = raw ^ 0x8000 (signed) / raw.  Lane L of a warp
+ * (channel L of a 32-channel block) always reads bank L: conflict-free for any activation codes.
+ * 16 KiB per (tap, 32-channel block); 0 when the shape is unsupported. */
+int64_t axb_depthwise_table_bytes(int64_t kh, int64_t kw, int64_t c);
+int axb_depthwise_table_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t coutp,
+                                const axb_lut *lut, uint32_t *d_table, void *stream);
 const char *axb_conv_variant_name(int variant);
 
 /* ---- small-channel layers: explicit im2col of the codes (axconv.py:160-196) ----

@@ -99,6 +99,8 @@ SIGNATURES = {
     "axb_ftable_c64_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "axb_ft_variant_layout": (c_int, [c_int]),
     "axb_depthwise_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),
+    "axb_depthwise_table_bytes": (c_i64, [c_i64, c_i64, c_i64]),
+    "axb_depthwise_table_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "axb_conv_variant_name": (ctypes.c_char_p, [c_int]),
     "axb_conv_im2col_kp": (c_i64, [c_i64, c_i64, c_i64]),
     "axb_im2col_pack": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,

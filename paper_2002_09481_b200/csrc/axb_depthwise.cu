@@ -14,8 +14,7 @@
 // channels of one pixel (coalesced code reads and fp32 stores), the b-major
 // table staged once per persistent CTA by TMA bulk copy.  Bank conflicts are
 // data-dependent (different rows b per lane, bank = (a>>1)&31).
-#include "axb_common.cuh"
-#include "axb_internal.h"
+#include "axb_convk.cuh"
 
 namespace axb {
 
@@ -35,6 +34,9 @@ struct DwK {
     int32_t *out_range, *flags;
     const uint16_t *lut;  // b-major
     int32_t sgn;
+    const uint32_t *dwtable;  // channel-bank table (axb_depthwise_table_prepare) or null
+    int32_t taps;
+    FastDiv fd_ow, fd_oh;
 };
 
 __device__ __forceinline__ uint32_t dw_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -106,9 +108,158 @@ __global__ void __launch_bounds__(1024, 1) depthwise_lut_kernel(const DwK p) {
                  AXB_FLAG_OUT_NONFINITE);
 }
 
+// ---------------------------------------------------------------- channel-bank table kernel
+// The filter codes of a depthwise layer are constants, so for each tap t and channel c only the 256
+// products lut[(a<<8) | b(t,c)] can occur.  They are laid out per 32-channel block cb as
+//     DW[cb][t][a >> 1][lane] = u(lut[(a_even<<8)|b]) | u(lut[(a_odd<<8)|b]) << 16,   lane = c % 32
+// (u = raw ^ 0x8000 for signed tables, raw for unsigned): 16 KiB per tap and block, 144 KiB for 3x3.
+// A warp = one output pixel x 32 channels, lane = channel; lane L always reads bank L, so every
+// LDS.32 is one wavefront (32 lookups) whatever the activation codes -- the b-major LUT the old
+// kernel reads conflicts on (a >> 1) & 31 across the 32 channels' codes.  The wanted half of the word
+// is picked with one PRMT whose selector comes from a & 1.  Persistent CTAs (one per SM) take
+// contiguous ranges of the (channel block, pixel) index space, so each CTA stages one or two
+// blocks' tables with TMA bulk copies; codes are read straight from the zp-padded NHWC code tensor
+// (32 contiguous bytes per warp and tap), outputs stored 128 B per warp.
+constexpr int kDwMaxTaps = 13;
+constexpr int kDwTapBytes = 128 * 32 * 4;  // 16 KiB
+
+__device__ __forceinline__ uint32_t dw_bias_word(int sgn) { return sgn ? 0x80008000u : 0u; }
+
+__global__ void dwtable_kernel(const uint8_t *__restrict__ fcodes, int taps, int c, int coutp,
+                               const uint16_t *__restrict__ lut_b, int sgn, uint32_t *__restrict__ out) {
+    const int nb = (c + 31) / 32;
+    const int64_t total = (int64_t)nb * taps * 128 * 32;
+    const uint32_t flip = sgn ? 0x8000u : 0u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int lane = (int)(i & 31);
+        const int a2 = (int)((i >> 5) & 127);
+        const int64_t r = i >> 12;
+        const int t = (int)(r % taps);
+        const int cb = (int)(r / taps);
+        const int ch = cb * 32 + lane;
+        uint32_t w = dw_bias_word(sgn);  // zero contribution (junk channels are never stored)
+        if (ch < c) {
+            const uint32_t b = fcodes[(int64_t)t * 16 * coutp + ch];  // (kh, kw, 1, c) view, cs 16
+            w = ((uint32_t)__ldg(lut_b + b * 256 + 2 * a2) ^ flip) |
+                (((uint32_t)__ldg(lut_b + b * 256 + 2 * a2 + 1) ^ flip) << 16);
+        }
+        out[i] = w;
+    }
+}
+
+template <int NW, int T>
+__global__ void __launch_bounds__(NW * 32, 1) depthwise_ct_kernel(const DwK p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int taps = T > 0 ? T : p.taps;
+    uint32_t *tab = reinterpret_cast<uint32_t *>(smem);
+    int32_t *tapoff = reinterpret_cast<int32_t *>(smem + kDwMaxTaps * kDwTapBytes);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(tapoff + 16);
+    const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) mbar_init(bar, 1);
+    if (tid < taps) tapoff[tid] = (int32_t)((((tid / p.kw) * p.dh) * p.wp + (tid % p.kw) * p.dw) * p.cs);
+    __syncthreads();
+
+    const double scale = p.inp->scale * p.fp->scale;
+    const int64_t zp1 = p.inp->zero_point, zp2 = p.fp->zero_point;
+    const int32_t kzz = (int32_t)(taps * zp1 * zp2);  // |.| <= 13 * 255 * 255
+    const int32_t ubias = p.sgn ? 32768 * taps : 0;
+    const int nb = (p.c + 31) / 32;
+    const int64_t M = p.n * p.oh * p.ow;
+    const int64_t total = (int64_t)nb * M;
+    const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
+    float tmin = INFINITY, tmax = -INFINITY;
+    int nonfinite = 0;
+    uint32_t phase = 0;
+    const uint8_t *tab_lane = smem + lane * 4;
+    for (int cb = lo < hi ? (int)(lo / M) : nb; cb < nb && (int64_t)cb * M < hi; ++cb) {
+        const int64_t s0 = max(lo, (int64_t)cb * M), s1 = min(hi, (int64_t)(cb + 1) * M);
+        // stage block cb's table; every thread's generic reads of the previous one precede the TMA write
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t bytes = (uint32_t)taps * kDwTapBytes;
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(smem, p.dwtable + (int64_t)cb * taps * (kDwTapBytes / 4), bytes, bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        const int ch = cb * 32 + lane;
+        const int chl = min(ch, p.c - 1);  // junk lanes of the last block read a real byte, store nothing
+        const int64_t fs = p.fsum[chl];
+        const float bias = p.bias ? __ldg(p.bias + chl) : 0.0f;
+        int32_t toff[T > 0 ? T : 1];
+#pragma unroll
+        for (int t = 0; t < T; ++t) toff[t] = tapoff[t];
+        // two pixels per warp iteration (independent loads in flight); 32-bit coordinates (M < 2^31)
+        const uint32_t e = (uint32_t)(s1 - (int64_t)cb * M);
+        for (uint32_t m0 = (uint32_t)(s0 - (int64_t)cb * M) + 2u * warp; m0 < e; m0 += 2u * NW) {
+            const uint8_t *src[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint32_t m = min(m0 + q, e - 1);
+                const uint32_t t1 = fdiv(m, p.fd_ow);
+                const uint32_t ox = m - t1 * (uint32_t)p.ow;
+                const uint32_t b = fdiv(t1, p.fd_oh);
+                const uint32_t oy = t1 - b * (uint32_t)p.oh;
+                src[q] = p.codes + (((int64_t)b * p.hp + oy * p.sh) * p.wp + (int64_t)ox * p.sw) * p.cs + chl;
+            }
+            uint32_t A[2] = {0, 0};
+            int32_t sp[2] = {0, 0};
+#pragma unroll
+            for (int t = 0; t < (T > 0 ? T : kDwMaxTaps); ++t) {
+                if (T == 0 && t >= taps) break;
+                const int32_t off = T > 0 ? toff[t] : tapoff[t];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const uint32_t a = __ldg(src[q] + off);
+                    const uint32_t w =
+                        *reinterpret_cast<const uint32_t *>(tab_lane + t * kDwTapBytes + (a >> 1) * 128u);
+                    A[q] += __byte_perm(w, 0, 0x4410u + (a & 1u) * 0x22u);  // the entry of code a
+                    sp[q] += p.sgn ? (int32_t)(int8_t)a : (int32_t)a;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (ch < p.c && m0 + q < e) {
+                    const int32_t Ai = (int32_t)A[q] - ubias;  // exact: |A| <= 13 * 32768
+                    const int64_t o = (int64_t)(m0 + q) * p.c + ch;
+                    if (p.acc_out) p.acc_out[o] = Ai;
+                    const int64_t corr = (int64_t)Ai - zp2 * sp[q] - zp1 * fs + kzz;  // axconv.py:249-254
+                    float y = __double2float_rn(scale * __ll2double_rn(corr));        // axconv.py:256
+                    if (p.bias) y = __fadd_rn(y, bias);                               // graph.py:268-269
+                    if (p.residual) y = __fadd_rn(y, __ldg(p.residual + o));          // graph.py:282-286
+                    if (p.relu) y = (y > 0.0f || y != y) ? y : 0.0f;                  // graph.py:276-277
+                    p.out[o] = y;
+                    track(y, tmin, tmax, nonfinite);
+                }
+            }
+        }
+    }
+    const bool any = tmin <= tmax;
+    range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
+                 AXB_FLAG_OUT_NONFINITE);
+}
+
 }  // namespace axb
 
 using namespace axb;
+
+extern "C" int64_t axb_depthwise_table_bytes(int64_t kh, int64_t kw, int64_t c) {
+    if (kh < 1 || kw < 1 || c < 1 || kh * kw > kDwMaxTaps) return 0;
+    return ((c + 31) / 32) * kh * kw * (int64_t)kDwTapBytes;
+}
+
+extern "C" int axb_depthwise_table_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t coutp,
+                                           const axb_lut *lut, uint32_t *d_table, void *stream) {
+    if (!d_fcodes || !lut || !d_table) return set_error(AXB_E_VALUE, "null argument");
+    if (axb_depthwise_table_bytes(kh, kw, c) == 0) return set_error(AXB_E_VALUE, "depthwise table: unsupported shape");
+    const int64_t words = axb_depthwise_table_bytes(kh, kw, c) / 4;
+    int64_t blocks = (words + 255) / 256;
+    if (blocks > (int64_t)sm_count() * 8) blocks = sm_count() * 8;
+    dwtable_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_fcodes, (int)(kh * kw), (int)c, (int)coutp,
+                                                                   lut->d_bmajor, lut->is_signed, d_table);
+    return check_launch("depthwise_table_prepare");
+}
 
 extern "C" int axb_depthwise_lut(const axb_conv_desc *d, const axb_lut *lut, void *stream) {
     if (!d || !lut) return set_error(AXB_E_VALUE, "null descriptor or table");
@@ -127,6 +278,33 @@ extern "C" int axb_depthwise_lut(const axb_conv_desc *d, const axb_lut *lut, voi
     k.out_range = d->out_range; k.flags = d->flags;
     k.lut = lut->d_bmajor;
     k.sgn = lut->is_signed;
+    k.taps = d->kh * d->kw;
+    if (d->ftable) {  // channel-bank table kernel (axb_depthwise_table_prepare)
+        if (k.taps > kDwMaxTaps) return set_error(AXB_E_VALUE, "depthwise table kernel: more than 13 taps");
+        k.dwtable = reinterpret_cast<const uint32_t *>(d->ftable);
+        if (d->n * d->oh * d->ow >= ((int64_t)1 << 31)) return set_error(AXB_E_VALUE, "depthwise conv too large");
+        k.fd_ow = make_fastdiv((uint32_t)d->ow);
+        k.fd_oh = make_fastdiv((uint32_t)d->oh);
+        constexpr int NW = 16;
+        const size_t smem = kDwMaxTaps * kDwTapBytes + 16 * 4 + 16;
+        auto fn = k.taps == 9 ? depthwise_ct_kernel<NW, 9> : depthwise_ct_kernel<NW, 0>;
+        static int configured[2] = {-1, -1};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int which = k.taps == 9;
+        if (configured[which] != dev) {
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for depthwise_ct_kernel");
+            configured[which] = dev;
+        }
+        const int64_t units = ((d->c + 31) / 32) * d->n * d->oh * d->ow;
+        int64_t grid = sm_count();
+        if (grid > (units + NW - 1) / NW) grid = (units + NW - 1) / NW;
+        if (grid < 1) grid = 1;
+        fn<<<(int)grid, NW * 32, smem, (cudaStream_t)stream>>>(k);
+        set_last_kernel("depthwise_ct");
+        return check_launch("depthwise_ct");
+    }
     const size_t smem = kLutBytes + 16;
     static int configured_dev = -1;
     int dev = 0;

@@ -94,9 +94,16 @@ class ConvLayer:
         c64_bytes = int(lib.axb_ftable_c64_bytes(self.kpad, self.coutp)) if self.has_ft else 0
         self.c64_ok = bool(c64_bytes and c64_bytes <= FTABLE_MAX_BYTES
                            and os.environ.get("AXB_FTABLE_C64", "1") != "0")
-        self.ftable = self.ftable_cm = self.ftable_c64 = None
+        self.ftable = self.ftable_cm = self.ftable_c64 = self.dwtable = None
         if self.has_ft:
             self.pair_table()
+        # depthwise: the channel-bank product table (axb_depthwise_table_prepare; conflict-free gathers)
+        dw_bytes = int(lib.axb_depthwise_table_bytes(self.kh, self.kw, self.cout)) if self.depthwise else 0
+        if dw_bytes and ftable:
+            self.dwtable = torch.empty(dw_bytes // 4, dtype=torch.int32, device=self.device)
+            _lib.check(lib.axb_depthwise_table_prepare(self.fcodes.data_ptr(), self.kh, self.kw, self.cout,
+                                                       self.coutp, self.lut.handle, self.dwtable.data_ptr(),
+                                                       torch.cuda.current_stream(self.device).cuda_stream))
         self.launches = 0
 
     def pair_table(self) -> torch.Tensor:
@@ -161,7 +168,8 @@ class ConvLayer:
 
     def table_bytes(self) -> int:
         """Device bytes held by this layer's product tables."""
-        return sum(t.numel() * 4 for t in (self.ftable, self.ftable_cm, self.ftable_c64) if t is not None)
+        return sum(t.numel() * 4 for t in (self.ftable, self.ftable_cm, self.ftable_c64, self.dwtable)
+                   if t is not None)
 
     def shares_codes_with(self, other: "ConvLayer") -> bool:
         """True when this layer can read ``other``'s code tensor of the same input instead of quantizing
@@ -298,7 +306,9 @@ class ConvLayer:
         d.variant = int(variant)
         d.pixel_order = int(pixel_order)
         table = None
-        if self.has_ft and use_ftable:
+        if self.depthwise and self.dwtable is not None and use_ftable:
+            table = self.dwtable
+        elif self.has_ft and use_ftable:
             lay = lib.axb_ft_variant_layout(int(ft_variant)) if ft_variant else 0
             table = self.cm_table() if lay == 1 else (self.c64_table() if lay == 2 else self.pair_table())
         d.ftable = table.data_ptr() if table is not None else None

@@ -48,7 +48,8 @@ def main():
         flags = torch.zeros(2, dtype=torch.int32, device="cuda")
         row = {"node": nid, "shape": list(x.shape), "filters": list(a["filters"].shape)}
         ref = None
-        for nm, v in list(names.items()) + [("lut_bmajor", -1)]:
+        cands = [("depthwise_ct", 0)] if layer.depthwise else list(names.items())
+        for nm, v in cands + [("lut_bmajor", -1)]:
             if v > 0 and not layer.layout_ok(v):
                 continue
             ts = []

@@ -423,9 +423,13 @@ def test_exact_lut_control_full_size_layer():
 
 
 @pytest.mark.parametrize("stride,shape,mode", [(1, (4, 28, 28, 32), O.SIGNED), (2, (4, 28, 28, 48), O.UNSIGNED),
-                                               (1, (2, 14, 14, 128), O.SIGNED)])
+                                               (1, (2, 14, 14, 128), O.SIGNED), (1, (2, 112, 112, 32), O.SIGNED),
+                                               (2, (2, 112, 112, 32), O.UNSIGNED), (1, (2, 56, 56, 128), O.UNSIGNED),
+                                               (2, (2, 56, 56, 128), O.SIGNED), (1, (3, 7, 9, 40), O.SIGNED)])
 def test_depthwise_matches_per_channel_oracle(stride, shape, mode):
-    """Config 5: depthwise approximate conv == per-channel axconv2d with shared ranges (bit-exact)."""
+    """Config 5: depthwise approximate conv == per-channel axconv2d with shared ranges (bit-exact), at the
+    MobileNet shapes (n,112,112,32) and (n,56,56,128), stride 1 and 2, ragged channel blocks (40, 48):
+    the channel-bank table kernel (depthwise_ct) and the b-major LUT kernel, outputs and raw sums."""
     torch = _torch()
     from paper_2002_09481_b200.layer import ConvLayer
     from paper_2002_09481_b200.types import ConvGeometry
@@ -443,8 +447,17 @@ def test_depthwise_matches_per_channel_oracle(stride, shape, mode):
                       depthwise=True)
     layer.set_input_params(*ir)
     flags = torch.zeros(2, dtype=torch.int32, device="cuda")
-    y = layer.run(torch.from_numpy(x).cuda(), None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr())
-    assert bits_equal(y.cpu().numpy(), want)
+    _, want_acc = O.depthwise_conv(x, f, ir, fr, lut, mode, padding="same", strides=(stride, stride),
+                                   return_acc=True)
+    from paper_2002_09481_b200 import _lib
+
+    for use_table, kern in ((True, "depthwise_ct"), (False, "depthwise_lut")):
+        acc = torch.empty(want_acc.shape, dtype=torch.int64, device="cuda")
+        y = layer.run(torch.from_numpy(x).cuda(), None, out_flag=flags[0].data_ptr(),
+                      quant_flag=flags[1].data_ptr(), use_ftable=use_table, acc_out=acc)
+        assert _lib.last_kernel() == kern
+        assert bits_equal(y.cpu().numpy(), want), kern
+        assert np.array_equal(acc.cpu().numpy(), want_acc), kern
 
 
 def test_quantizer_fast_path_sweep():
