@@ -38,6 +38,12 @@ struct ConvK {
     int32_t sp_inloop;  // 1: patch sums accumulated in the chunk loop (dp4a), 0: gathered in the epilogue
     const uint32_t *ftable;  // filter-specialised product table (axb_ftable_prepare), or null
     int32_t ntm;             // pixel tiles per channel block (ftable kernel: tile = nb * ntm + mt)
+    // tail split (c64 kernel): the last split_L tiles are cut into split_s K-ranges (chunk-aligned pieces)
+    // dealt piece-major over the CTAs; partial sums go to split_ws, the last piece of a tile to arrive
+    // on split_cnt reduces them and runs the epilogue (0 / 1: no split)
+    int32_t split_L, split_s;
+    uint32_t *split_ws;
+    int32_t *split_cnt;
 };
 
 // ---------------------------------------------------------------- PTX helpers

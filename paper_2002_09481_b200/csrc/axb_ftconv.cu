@@ -38,6 +38,8 @@
 //
 // Tiles: BM = WARPS*32*TM output pixels x BN = 2*NPB channels; tile = nb * ntm + mt, so
 // the CTAs running concurrently share one channel block's table rows in L2.
+#include <cstdlib>
+
 #include "axb_convk.cuh"
 
 namespace axb {
@@ -627,8 +629,10 @@ constexpr int kC64RowBytes = kC64RowWords * 4;  // 32 KiB
 __host__ __device__ constexpr int c64_stage_bytes(int KS) { return KS * kC64RowBytes; }
 __host__ __device__ constexpr int c64_codebuf_bytes(int WARPS, int J) { return WARPS * 2 * 4 * J * 16; }
 __host__ __device__ constexpr int c64_smem(int KS, int ST, int WARPS, int J) {
-    return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS, J) + kMaxTaps * 4 + 2 * ST * 8;
+    return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS, J) + kMaxTaps * 4 + 2 * ST * 8 + 16;
 }
+// tail-split workspace: 32-bit words per thread for one piece's partial sums (acc_all, acc_hi, S_p)
+__host__ __device__ constexpr int c64_split_words(int J) { return 8 * J + (4 * J) / 32; }
 
 template <int J, int WARPS, int KS, int ST, bool SGN, int CR>
 __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
@@ -639,7 +643,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     constexpr int BN = 64;
     constexpr int SPG = CR / KS;      // stages per CR-row code group
     constexpr int NG = 16 / CR;       // code groups per 16-row chunk
+    constexpr int SPCH = 16 / KS;     // stages per 16-row chunk
     constexpr int CBW = PXW * 16;     // one of a warp's two code buffers (bytes)
+    constexpr int WPT = c64_split_words(J);
     constexpr uint32_t STAGE_BYTES = c64_stage_bytes(KS);
     static_assert(PXW % 32 == 0, "whole 32-pixel groups per warp (J = 8 or 16)");
     static_assert(CR == 4 || CR == 8, "code rows per register load: 4 (LDS.32) or 8 (LDS.64)");
@@ -652,6 +658,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     int32_t *tapoff_s = reinterpret_cast<int32_t *>(codebuf + c64_codebuf_bytes(WARPS, J));
     uint64_t *full = reinterpret_cast<uint64_t *>(tapoff_s + kMaxTaps);
     uint64_t *empty = full + ST;
+    int32_t *last_s = reinterpret_cast<int32_t *>(empty + ST);  // tail split: "this CTA reduces the tile"
 
     const int tid = (int)threadIdx.x;
     const int lane = tid & 31;
@@ -667,29 +674,55 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     for (int t = tid; t < p.taps; t += NT) tapoff_s[t] = ((t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw) * p.cs;
     __syncthreads();
 
-    // 32-bit loop state throughout (registers are the budget here; the host guarantees
-    // ntiles * stages-per-tile < 2^31)
+    // ---- work items (32-bit loop state throughout: registers are the budget here; the host guarantees
+    // ntiles * stages-per-tile < 2^31).  Items 0 .. n_full-1: whole tiles cid, cid+grid, ... of the first
+    // T - L tiles (channel-block-major, so concurrently running CTAs share one block's table rows in L2);
+    // then the tail: pieces i = cid, cid+grid, ... of the last L tiles x S chunk ranges, piece-major
+    // (i = piece * L + tile), so concurrent CTAs again read the same table rows.
     const int grid = (int)gridDim.x;
     const int cid = (int)blockIdx.x;
-    const int my_tiles = p.ntiles > cid ? (int)((p.ntiles - cid + grid - 1) / grid) : 0;
-    const int spt = p.nchunks * (16 / KS);  // stages per tile
-    const int total = my_tiles * spt;
-
-    int pr_h = 0, pr_q = 0, pr_tile = cid, pr_slot = 0;
-    auto produce = [&]() {
-        const int nb = pr_tile / p.ntm;
-        mbar_expect_tx(full + pr_slot, STAGE_BYTES);
-        bulk_g2s(smem + pr_slot * STAGE_BYTES,
-                 p.ftable + ((int64_t)nb * p.kpad + pr_q * KS) * kC64RowWords, STAGE_BYTES, full + pr_slot);
-        ++pr_h;
-        if (++pr_slot == ST) pr_slot = 0;
-        if (++pr_q == spt) {
-            pr_q = 0;
-            pr_tile += grid;
+    const int T = (int)p.ntiles;
+    const int L = p.split_s > 1 ? p.split_L : 0;
+    const int S = p.split_s > 1 ? p.split_s : 1;
+    const int Tfull = T - L;
+    const int n_full = Tfull > cid ? (Tfull - cid + grid - 1) / grid : 0;
+    const int n_items = n_full + (L * S > cid ? (L * S - cid + grid - 1) / grid : 0);
+    // item k -> tile, chunk range [kcb, kce), piece (-1: whole tile)
+    auto item = [&](int k, int &tile, int &kcb, int &kce, int &pc) {
+        if (k < n_full) {
+            tile = cid + k * grid;
+            kcb = 0;
+            kce = p.nchunks;
+            pc = -1;
+        } else {
+            const int i = cid + (k - n_full) * grid;
+            pc = i / L;
+            tile = Tfull + (i - pc * L);
+            kcb = pc * p.nchunks / S;
+            kce = (pc + 1) * p.nchunks / S;
         }
     };
-    if (tid == 0)
-        for (int s = 0; s < ST - 1 && pr_h < total; ++s) produce();
+
+    // ---- producer (thread 0): stage -> KS rows [pr_q*KS, +KS) of channel block pr_nb
+    int pr_k = 0, pr_q = 0, pr_qe = 0, pr_nb = 0, pr_slot = 0;
+    auto pr_item = [&]() {
+        int t, b, e, pc;
+        item(pr_k, t, b, e, pc);
+        pr_q = b * SPCH;
+        pr_qe = e * SPCH;
+        pr_nb = t / p.ntm;
+    };
+    auto produce = [&]() {  // requires pr_k < n_items
+        mbar_expect_tx(full + pr_slot, STAGE_BYTES);
+        bulk_g2s(smem + pr_slot * STAGE_BYTES,
+                 p.ftable + ((int64_t)pr_nb * p.kpad + pr_q * KS) * kC64RowWords, STAGE_BYTES, full + pr_slot);
+        if (++pr_slot == ST) pr_slot = 0;
+        if (++pr_q == pr_qe && ++pr_k < n_items) pr_item();
+    };
+    if (tid == 0 && n_items > 0) {
+        pr_item();
+        for (int s = 0; s < ST - 1 && pr_k < n_items; ++s) produce();
+    }
 
     // ---- code loader: lane L stages pixels L, L+32, ... (of this warp's PXW) one 16-row chunk ahead
     uint8_t *wbuf = codebuf + warp * (2 * CBW);
@@ -704,25 +737,29 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
         }
     };
     pdl_wait();
-    int ld_t = 0, ld_ci = 0, ld_kc = 0, ld_buf = 0;
-    int ld_left = my_tiles * p.nchunks, ld_tile = cid;
+    int ld_k = 0, ld_kc = 0, ld_ke = 0, ld_t = 0, ld_ci = 0, ld_buf = 0;
+    auto ld_item = [&]() {
+        int t, b, e, pc;
+        item(ld_k, t, b, e, pc);
+        const int cpt = p.cs >> 4;  // chunks per tap
+        ld_kc = b;
+        ld_ke = e;
+        ld_t = b / cpt;
+        ld_ci = (b - ld_t * cpt) * 16;
+        set_row(t);
+    };
     auto load_next = [&]() {
-        if (ld_left > 0) {
+        if (ld_k < n_items) {
             const int off = tapoff_s[ld_t] + ld_ci;
 #pragma unroll
             for (int i = 0; i < NPL; ++i)
                 cp_async16(wbuf + ld_buf * CBW + (lane + 32 * i) * 16, p.codes + rowbase[i] + off, 16);
-            --ld_left;
             ld_ci += 16;
             if (ld_ci == p.cs) {
                 ld_ci = 0;
                 ++ld_t;
             }
-            if (++ld_kc == p.nchunks) {
-                ld_kc = ld_t = ld_ci = 0;
-                ld_tile += grid;
-                if (ld_left > 0) set_row(ld_tile);
-            }
+            if (++ld_kc == ld_ke && ++ld_k < n_items) ld_item();
         }
         ld_buf ^= 1;
         cp_async_commit();  // one group per chunk (possibly empty), so wait_group<1> tracks chunk c
@@ -742,16 +779,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
 
     int g = 0, slot = 0;
     uint32_t phase = 0;
-    int c_tile = cid;
     int cbuf = 0;
-    if (my_tiles > 0) {
-        set_row(c_tile);
+    if (n_items > 0) {
+        ld_item();
         load_next();
     }
     const uint8_t *tab_lane = smem + o * 16;
-    for (int jt = 0; jt < my_tiles; ++jt) {
+    for (int kk = 0; kk < n_items; ++kk) {
+        int c_tile, kcb, kce, pc;
+        item(kk, c_tile, kcb, kce, pc);
 #pragma unroll 1
-        for (int kc = 0; kc < p.nchunks; ++kc) {
+        for (int kc = kcb; kc < kce; ++kc) {
             __syncwarp();   // every lane is done reading the buffer the next copy overwrites
             load_next();    // chunk kc+1 -> the other buffer
             cp_async_wait<1>();
@@ -772,7 +810,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
                     spl[i] = (int32_t)__dp4a(mine.w, 0x01010101u, t);
                 }
             }
-#pragma unroll
+#pragma unroll 1
             for (int gr = 0; gr < NG; ++gr) {
                 uint32_t cur[J][CR / 4];
 #pragma unroll
@@ -788,7 +826,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
                 }
 #pragma unroll
                 for (int st = 0; st < SPG; ++st) {
-                    if (tid == 0 && pr_h < total) {
+#ifndef AXB_EXP_C64_NOREFILL
+                    if (tid == 0 && pr_k < n_items) {
                         // refill the slot stage g-1 used once every warp released it
                         if (g >= 1) {
                             const int ps_ = slot == 0 ? ST - 1 : slot - 1;
@@ -798,6 +837,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
                         produce();
                     }
                     mbar_wait(full + slot, phase);
+#else  // A/B experiment only (wrong products): the first ST-1 stages are loaded once and never refilled
+                    if (g < ST - 1) mbar_wait(full + slot, phase);
+#endif
                     const uint8_t *stab = tab_lane + slot * STAGE_BYTES;
 #pragma unroll
                     for (int kl = 0; kl < KS; ++kl) {
@@ -823,6 +865,55 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
                 }
             }
             cbuf ^= 1;
+        }
+
+        if (pc >= 0) {
+            // ---- tail split: publish this piece's partial sums; the last piece to arrive adds the
+            // others and runs the epilogue (exact: all/S_p mod 2^32, hi < 2^32 for kpad <= 65536)
+            const int ti = c_tile - Tfull;
+            uint32_t *mine = p.split_ws + ((int64_t)ti * S + pc) * (WPT * NT) + tid;
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    mine[(8 * j + r) * NT] = acc_all[j][r];
+                    mine[(8 * j + 4 + r) * NT] = acc_hi[j][r];
+                }
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) mine[(8 * J + i) * NT] = (uint32_t)spl[i];
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                const int last = atomicAdd(p.split_cnt + ti, 1) == S - 1;
+                if (last) p.split_cnt[ti] = 0;  // every piece arrived: ready for the next launch
+                *last_s = last;
+            }
+            __syncthreads();
+            const bool last = *last_s != 0;
+            __syncthreads();  // everyone read the flag before a later item rewrites it
+            if (!last) {
+#pragma unroll
+                for (int j = 0; j < J; ++j)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc_all[j][r] = acc_hi[j][r] = 0;
+#pragma unroll
+                for (int i = 0; i < NPL; ++i) spl[i] = 0;
+                continue;
+            }
+            __threadfence();
+            for (int q = 0; q < S; ++q) {
+                if (q == pc) continue;
+                const uint32_t *other = p.split_ws + ((int64_t)ti * S + q) * (WPT * NT) + tid;
+#pragma unroll
+                for (int j = 0; j < J; ++j)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        acc_all[j][r] += __ldcg(other + (8 * j + r) * NT);
+                        acc_hi[j][r] += __ldcg(other + (8 * j + 4 + r) * NT);
+                    }
+#pragma unroll
+                for (int i = 0; i < NPL; ++i) spl[i] += (int32_t)__ldcg(other + (8 * J + i) * NT);
+            }
         }
 
         // ------------------------------------------------ fused epilogue (same arithmetic as lutconv_ft)
@@ -899,7 +990,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
 #pragma unroll
             for (int i = 0; i < NPL; ++i) spl[i] = 0;
         }
-        c_tile += grid;
     }
     cp_async_wait<0>();
     const bool any = tmin <= tmax;
@@ -1053,6 +1143,52 @@ static int launch_ftcm(int op, const ConvK &k, int sm_limit, cudaStream_t s, con
     return check_launch("lutconv_ftcm");
 }
 
+// Tail split plan for a persistent grid of G CTAs over T whole tiles of nch 16-row chunks: the last L tiles
+// (the partial wave, optionally plus one full wave) are cut into s chunk-aligned K pieces dealt over all
+// CTAs, minimising the finishing time in tile units: (T - L) / G + ceil(L * s / G) / s (+2% per extra
+// piece round for the partial-sum traffic).  L = 0: no split.
+static void tail_split_plan(int64_t T, int64_t G, int nch, int &L, int &S) {
+    L = 0;
+    S = 1;
+    if (T <= 0 || G <= 1) return;
+    const int64_t r = T % G;
+    if (r == 0) return;
+    double best = (double)((T + G - 1) / G);
+    for (int m = 0; m <= 1; ++m) {
+        const int64_t Lc = r + m * G;
+        if (Lc > T) break;
+        for (int sc = 2; sc <= 8 && sc <= nch; ++sc) {
+            const int64_t rounds = (Lc * sc + G - 1) / G;
+            const double t = (double)((T - Lc) / G) + (double)rounds / sc + 0.02 * rounds;
+            if (t < best - 1e-9) {
+                best = t;
+                L = (int)Lc;
+                S = sc;
+            }
+        }
+    }
+}
+// stream-ordered scratch comes from the device's default pool; keep freed blocks in the pool (no release
+// to the OS at every synchronisation) so per-launch workspaces cost no driver allocation
+static void keep_pool_memory(int dev) {
+    static int done_mask = 0;
+    if (dev < 0 || dev >= 31 || (done_mask >> dev) & 1) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done_mask |= 1 << dev;
+}
+static bool c64_split_enabled() {
+    static const int on = [] {
+        const char *e = getenv("AXB_C64_SPLIT");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return on != 0;
+}
+
 template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3, int CR = 8>
 static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WARPS * 4 * J;
@@ -1077,6 +1213,25 @@ static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, co
     int64_t nblk = sm_limit > 0 ? sm_limit : sm_count();
     if (nblk > kk.ntiles) nblk = kk.ntiles;
     if (nblk < 1) nblk = 1;
+    // tail split: cut the last wave's tiles into K pieces so every CTA ends at about the same time
+    int split_L = 0, split_s = 1;
+    if (c64_split_enabled()) tail_split_plan(kk.ntiles, nblk, k.nchunks, split_L, split_s);
+    kk.split_L = split_L;
+    kk.split_s = split_s;
+    void *ws = nullptr;
+    if (split_s > 1) {
+        keep_pool_memory(dev);
+        const size_t ws_bytes = (size_t)split_L * split_s * (WARPS * 32) * c64_split_words(J) * 4;
+        const size_t cnt_bytes = (size_t)split_L * 4;
+        if (cudaMallocAsync(&ws, ws_bytes + cnt_bytes, s) != cudaSuccess)
+            return set_error(AXB_E_CUDA, "cannot allocate the c64 tail-split workspace");
+        kk.split_ws = static_cast<uint32_t *>(ws);
+        kk.split_cnt = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(ws) + ws_bytes);
+        if (cudaMemsetAsync(kk.split_cnt, 0, cnt_bytes, s) != cudaSuccess) {
+            cudaFreeAsync(ws, s);
+            return set_error(AXB_E_CUDA, "cannot clear the c64 tail-split counters");
+        }
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1086,8 +1241,10 @@ static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, co
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, fn, kk) != cudaSuccess) return check_launch("lutconv_ftc64");
+    cfg.numAttrs = ws ? 0 : 1;  // PDL only without the memset in between
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, fn, kk);
+    if (ws) cudaFreeAsync(ws, s);
+    if (le != cudaSuccess) return check_launch("lutconv_ftc64");
     set_last_kernel(name);
     return check_launch("lutconv_ftc64");
 }
