@@ -923,6 +923,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
             const int64_t m0 = (int64_t)(c_tile % p.ntm) * BM;
             const int cb = nb * BN + o * 8;  // this lane's 8 channels
             const bool full_blk = cb + 8 <= p.cout && (p.cout & 3) == 0;
+            const bool has_res = p.residual != nullptr, relu = p.relu != 0;
+            // per-channel terms hoisted out of the pixel loop: -zp1*S_f + K*zp1*zp2 - (entry bias), and the
+            // bias (-0.0f when absent: x + -0 == x for every float, so the add is an exact identity)
+            int64_t cc[8];
+            float bv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const bool ok = full_blk || cb + t < p.cout;
+                cc[t] = ok ? e.kzz - e.zp1 * __ldg(p.fsum + cb + t) - bias_units : 0;
+                bv[t] = (ok && p.bias) ? __ldg(p.bias + cb + t) : -0.0f;
+            }
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int32_t spj = __shfl_sync(0xffffffffu, spl[j >> 3], (j * 4 + ps) & 31);
@@ -932,55 +943,53 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
                     const int64_t m = pixel_of(p, mt, pix0);
                     const int64_t pz = -e.zp2 * (int64_t)spj;
                     float *dst = p.out + m * p.cout + cb;
+                    // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254), A = sum u - bias_units;
+                    // fp64 dequant (:256), bias (graph.py:268-269), Add (:282-286), ReLU (:276-277)
+                    float y[8];
 #pragma unroll
-                    for (int hq = 0; hq < 2; ++hq) {
-                        int64_t A[4];
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const uint32_t hi = acc_hi[j][2 * hq + h];
-                            const uint32_t lo = acc_all[j][2 * hq + h] - (hi << 16);
-                            A[2 * h] = (int64_t)lo - bias_units;
-                            A[2 * h + 1] = (int64_t)hi - bias_units;
+                    for (int h = 0; h < 4; ++h) {
+                        const uint32_t hi = acc_hi[j][h];
+                        const uint32_t lo = acc_all[j][h] - (hi << 16);
+                        y[2 * h] = __fadd_rn(__double2float_rn(e.scale * __ll2double_rn((int64_t)lo + (pz + cc[2 * h]))),
+                                             bv[2 * h]);
+                        y[2 * h + 1] = __fadd_rn(
+                            __double2float_rn(e.scale * __ll2double_rn((int64_t)hi + (pz + cc[2 * h + 1]))), bv[2 * h + 1]);
+                    }
+                    if (full_blk) {
+                        if (has_res) {
+                            const float4 r0 = __ldg(reinterpret_cast<const float4 *>(p.residual + m * p.cout + cb));
+                            const float4 r1 = __ldg(reinterpret_cast<const float4 *>(p.residual + m * p.cout + cb + 4));
+                            y[0] = __fadd_rn(y[0], r0.x); y[1] = __fadd_rn(y[1], r0.y);
+                            y[2] = __fadd_rn(y[2], r0.z); y[3] = __fadd_rn(y[3], r0.w);
+                            y[4] = __fadd_rn(y[4], r1.x); y[5] = __fadd_rn(y[5], r1.y);
+                            y[6] = __fadd_rn(y[6], r1.z); y[7] = __fadd_rn(y[7], r1.w);
                         }
-                        const int c0 = cb + 4 * hq;
-                        if (full_blk) {
-                            float y[4];
 #pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254); fp64 dequant (:256)
-                                const int64_t corr = A[t] + pz - e.zp1 * __ldg(p.fsum + c0 + t) + e.kzz;
-                                y[t] = __double2float_rn(e.scale * __ll2double_rn(corr));
-                                if (p.bias) y[t] = __fadd_rn(y[t], __ldg(p.bias + c0 + t));  // graph.py:268-269
-                            }
-                            if (p.residual) {  // graph.py:282-286
-                                const float4 r = __ldg(reinterpret_cast<const float4 *>(p.residual + m * p.cout + c0));
-                                y[0] = __fadd_rn(y[0], r.x); y[1] = __fadd_rn(y[1], r.y);
-                                y[2] = __fadd_rn(y[2], r.z); y[3] = __fadd_rn(y[3], r.w);
-                            }
+                        for (int t = 0; t < 8; ++t) {
+                            if (relu) y[t] = (y[t] > 0.0f || y[t] != y[t]) ? y[t] : 0.0f;  // np.maximum(x, 0)
+                            track(y[t], tmin, tmax, nonfinite);
+                        }
+                        *reinterpret_cast<float4 *>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+                        *reinterpret_cast<float4 *>(dst + 4) = make_float4(y[4], y[5], y[6], y[7]);
+                    } else {
 #pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                if (p.relu) y[t] = (y[t] > 0.0f || y[t] != y[t]) ? y[t] : 0.0f;  // np.maximum(x, 0)
-                                track(y[t], tmin, tmax, nonfinite);
+                        for (int t = 0; t < 8; ++t) {
+                            if (cb + t < p.cout) {
+                                float v = y[t];
+                                if (has_res) v = __fadd_rn(v, p.residual[m * p.cout + cb + t]);
+                                if (relu) v = (v > 0.0f || v != v) ? v : 0.0f;
+                                track(v, tmin, tmax, nonfinite);
+                                dst[t] = v;
                             }
-                            *reinterpret_cast<float4 *>(dst + 4 * hq) = make_float4(y[0], y[1], y[2], y[3]);
-                            if (p.acc_out) {
+                        }
+                    }
+                    if (p.acc_out) {
 #pragma unroll
-                                for (int t = 0; t < 4; ++t) p.acc_out[m * p.cout + c0 + t] = A[t];
-                            }
-                        } else {
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                if (c0 + t < p.cout) {
-                                    const int64_t corr = A[t] + pz - e.zp1 * p.fsum[c0 + t] + e.kzz;
-                                    float v = __double2float_rn(e.scale * __ll2double_rn(corr));
-                                    if (p.bias) v = __fadd_rn(v, p.bias[c0 + t]);
-                                    if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + c0 + t]);
-                                    if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;
-                                    track(v, tmin, tmax, nonfinite);
-                                    dst[4 * hq + t] = v;
-                                    if (p.acc_out) p.acc_out[m * p.cout + c0 + t] = A[t];
-                                }
-                            }
+                        for (int h = 0; h < 4; ++h) {
+                            const uint32_t hi = acc_hi[j][h];
+                            const uint32_t lo = acc_all[j][h] - (hi << 16);
+                            if (cb + 2 * h < p.cout) p.acc_out[m * p.cout + cb + 2 * h] = (int64_t)lo - bias_units;
+                            if (cb + 2 * h + 1 < p.cout) p.acc_out[m * p.cout + cb + 2 * h + 1] = (int64_t)hi - bias_units;
                         }
                     }
                 }
