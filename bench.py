@@ -426,14 +426,15 @@ def device_rank(args, spec, batch, ctx, units) -> dict:
 
     # warm-up (also prepares filters once: hoisted quantize_filters), per-layer kernel autotune on the
     # first batch (outside the timed region; bit-identity of all variants checked), CUDA-graph capture
+    tuned = {}
+    if graphs and args.tuned_from:  # replay an earlier run's picks (e.g. under ncu, whose replays distort
+        # timing) from the first warm-up on, so a launch list / traffic capture sees only the tuned kernels
+        graphs[0].set_tuning(json.loads(Path(args.tuned_from).read_text()))
+        tuned = {"from": args.tuned_from}
     for _ in range(args.warmup):
         run_all(x_dev, check=True)
-    tuned = {}
     if graphs:
-        if args.tuned_from:  # replay an earlier run's picks (e.g. under ncu, whose replays distort timing)
-            graphs[0].set_tuning(json.loads(Path(args.tuned_from).read_text()))
-            tuned = {"from": args.tuned_from}
-        elif not args.no_autotune:
+        if not args.tuned_from and not args.no_autotune:
             tuned = graphs[0].autotune(x_dev)
             if args.tuned_out:
                 Path(args.tuned_out).write_text(json.dumps(graphs[0].tuning()))

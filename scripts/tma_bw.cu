@@ -201,7 +201,8 @@ int main() {
     cudaMalloc(&sink, 4096);
     cudaMemset(src, 1, 512ull << 20);
     const int cfgs[][4] = {{3, 64, 1, 4}, {3, 64, 1, 36}, {6, 32, 1, 36}, {12, 16, 1, 36}, {3, 64, 1, 68},
-                           {6, 32, 1, 68}, {2, 96, 1, 36}, {4, 48, 1, 36}};
+                           {6, 32, 1, 68}, {2, 96, 1, 36}, {4, 48, 1, 36}, {3, 64, 1, 37}, {6, 32, 1, 37},
+                           {2, 96, 1, 37}, {3, 64, 4, 36}, {6, 32, 2, 36}};
     for (auto &c : cfgs) {
         h_ST = c[0], h_STAGE = c[1] * 1024u, h_CHUNKS = c[2], h_MODE = c[3];
         run<1>(src, bytes, 1, sink, nsm);
