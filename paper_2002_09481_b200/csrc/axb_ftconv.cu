@@ -632,13 +632,16 @@ __host__ __device__ constexpr int c64_smem(int KS, int ST, int WARPS, int J) {
     return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS, J) + kMaxTaps * 4 + 2 * ST * 8 + 16;
 }
 // tail-split workspace: 32-bit words per thread for one piece's partial sums (acc_all, acc_hi, S_p)
-__host__ __device__ constexpr int c64_split_words(int J) { return 8 * J + (4 * J) / 32; }
+__host__ __device__ constexpr int c64_split_words(int J) { return 8 * J + (4 * J + 31) / 32; }
 
-template <int J, int WARPS, int KS, int ST, bool SGN, int CR>
-__global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
-    constexpr int NT = WARPS * 32;
+// PW = 1: an extra warpgroup whose first thread is the TMA producer (it refills a slot the moment the
+// last consumer warp released it); it gives its registers to the consumers (setmaxnreg).  PW = 0: thread 0
+// refills the previous stage's slot at the start of each stage.
+template <int J, int WARPS, int KS, int ST, bool SGN, int CR, int PW>
+__global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_ftc64(const ConvK p) {
+    constexpr int NT = WARPS * 32;  // consumer threads
     constexpr int PXW = 4 * J;        // pixels per warp
-    constexpr int NPL = PXW / 32;     // pixels whose codes each lane stages
+    constexpr int NPL = (PXW + 31) / 32;  // pixels whose codes each lane stages (the last slot may be partial)
     constexpr int BM = WARPS * PXW;
     constexpr int BN = 64;
     constexpr int SPG = CR / KS;      // stages per CR-row code group
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     constexpr int CBW = PXW * 16;     // one of a warp's two code buffers (bytes)
     constexpr int WPT = c64_split_words(J);
     constexpr uint32_t STAGE_BYTES = c64_stage_bytes(KS);
-    static_assert(PXW % 32 == 0, "whole 32-pixel groups per warp (J = 8 or 16)");
+    static_assert(PXW % 16 == 0, "whole 16-pixel groups per warp (J = 8, 12, 16, 20, ...)");
     static_assert(CR == 4 || CR == 8, "code rows per register load: 4 (LDS.32) or 8 (LDS.64)");
     static_assert(KS == 1 || KS == 2 || KS == 4, "KS rows per stage: 1, 2 or 4");
     static_assert(CR % KS == 0, "a stage never straddles two code groups");
@@ -671,7 +674,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
             mbar_init(empty + s, WARPS);
         }
     }
-    for (int t = tid; t < p.taps; t += NT) tapoff_s[t] = ((t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw) * p.cs;
+    for (int t = tid; t < p.taps; t += (int)blockDim.x) tapoff_s[t] = ((t / p.kw) * p.dh * p.wp + (t % p.kw) * p.dw) * p.cs;
     __syncthreads();
 
     // ---- work items (32-bit loop state throughout: registers are the budget here; the host guarantees
@@ -719,10 +722,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
         if (++pr_slot == ST) pr_slot = 0;
         if (++pr_q == pr_qe && ++pr_k < n_items) pr_item();
     };
-    if (tid == 0 && n_items > 0) {
+    if (!PW && tid == 0 && n_items > 0) {
         pr_item();
         for (int s = 0; s < ST - 1 && pr_k < n_items; ++s) produce();
     }
+    auto consumers_sync = [&]() {
+        if constexpr (PW) asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+        else __syncthreads();
+    };
 
     // ---- code loader: lane L stages pixels L, L+32, ... (of this warp's PXW) one 16-row chunk ahead
     uint8_t *wbuf = codebuf + warp * (2 * CBW);
@@ -753,7 +760,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
             const int off = tapoff_s[ld_t] + ld_ci;
 #pragma unroll
             for (int i = 0; i < NPL; ++i)
-                cp_async16(wbuf + ld_buf * CBW + (lane + 32 * i) * 16, p.codes + rowbase[i] + off, 16);
+                if (PXW % 32 == 0 || lane + 32 * i < PXW)
+                    cp_async16(wbuf + ld_buf * CBW + (lane + 32 * i) * 16, p.codes + rowbase[i] + off, 16);
             ld_ci += 16;
             if (ld_ci == p.cs) {
                 ld_ci = 0;
@@ -780,6 +788,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
     int g = 0, slot = 0;
     uint32_t phase = 0;
     int cbuf = 0;
+    if constexpr (PW) {
+        static_assert(WARPS % 4 == 0, "consumer warpgroups");
+        if (warp >= WARPS) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 240;\n" ::: "memory");
+    }
+    if (PW && warp >= WARPS) {
+        // ---- dedicated producer: stage h goes into slot h % ST once the consumers released stage h - ST
+        if (warp == WARPS && lane == 0 && n_items > 0) {
+            pr_item();
+            for (int h = 0; pr_k < n_items; ++h) {
+                if (h >= ST) mbar_wait(empty + pr_slot, (uint32_t)((h / ST) - 1) & 1u);
+                produce();
+            }
+        }
+    } else {
     if (n_items > 0) {
         ld_item();
         load_next();
@@ -797,6 +820,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
             const uint8_t *cb_ = wbuf + cbuf * CBW;
 #pragma unroll
             for (int i = 0; i < NPL; ++i) {  // S_p of the staged pixels (axconv.py:193; junk codes are raw 0)
+                if (PXW % 32 != 0 && lane + 32 * i >= PXW) continue;
                 const uint4 mine = *reinterpret_cast<const uint4 *>(cb_ + (lane + 32 * i) * 16);
                 if (SGN) {
                     spl[i] = __dp4a((int)mine.x, 0x01010101, spl[i]);
@@ -827,7 +851,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
 #pragma unroll
                 for (int st = 0; st < SPG; ++st) {
 #ifndef AXB_EXP_C64_NOREFILL
-                    if (tid == 0 && pr_k < n_items) {
+                    if (!PW && tid == 0 && pr_k < n_items) {
                         // refill the slot stage g-1 used once every warp released it
                         if (g >= 1) {
                             const int ps_ = slot == 0 ? ST - 1 : slot - 1;
@@ -882,15 +906,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
 #pragma unroll
             for (int i = 0; i < NPL; ++i) mine[(8 * J + i) * NT] = (uint32_t)spl[i];
             __threadfence();
-            __syncthreads();
+            consumers_sync();
             if (tid == 0) {
                 const int last = atomicAdd(p.split_cnt + ti, 1) == S - 1;
                 if (last) p.split_cnt[ti] = 0;  // every piece arrived: ready for the next launch
                 *last_s = last;
             }
-            __syncthreads();
+            consumers_sync();
             const bool last = *last_s != 0;
-            __syncthreads();  // everyone read the flag before a later item rewrites it
+            consumers_sync();  // everyone read the flag before a later item rewrites it
             if (!last) {
 #pragma unroll
                 for (int j = 0; j < J; ++j)
@@ -1000,6 +1024,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftc64(const ConvK p) {
             for (int i = 0; i < NPL; ++i) spl[i] = 0;
         }
     }
+    }  // consumers
     cp_async_wait<0>();
     const bool any = tmin <= tmax;
     range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
@@ -1112,6 +1137,10 @@ static const FtVariant kFtVariants[] = {
     {"c64_j8_w8_k2", 8, 8, 32, 1, 1.000f, 2},
     {"c64_j8_w16_k1", 8, 16, 32, 1, 1.000f, 2},
     {"c64_j16_w8_k2", 16, 8, 32, 1, 1.000f, 2},
+    {"c64_j16_w8_k2_pw", 16, 8, 32, 1, 1.000f, 2},
+    {"c64_j20_w8_k2_pw", 20, 8, 32, 1, 1.000f, 2},
+    {"c64_j20_w8_k2_pw_c4", 20, 8, 32, 1, 1.000f, 2},
+    {"c64_j16_w8_k2_pw_c4", 16, 8, 32, 1, 1.000f, 2},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
@@ -1198,12 +1227,12 @@ static bool c64_split_enabled() {
     return on != 0;
 }
 
-template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3, int CR = 8>
+template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3, int CR = 8, int PW = 0>
 static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WARPS * 4 * J;
     constexpr int BN = 64;
     const size_t smem = c64_smem(KS, ST, WARPS, J);
-    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN, CR>;
+    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN, CR, PW>;
     static int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1246,7 +1275,7 @@ static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, co
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.gridDim = dim3((unsigned)nblk);
-    cfg.blockDim = dim3(WARPS * 32);
+    cfg.blockDim = dim3(WARPS * 32 + PW * 128);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
@@ -1334,6 +1363,10 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 17: return launch_ftc64<8, 8, SGN>(op, k, sm_limit, s, nm);
         case 18: return launch_ftc64<8, 16, SGN, 1, 6>(op, k, sm_limit, s, nm);
         case 19: return launch_ftc64<16, 8, SGN, 2, 3, 8>(op, k, sm_limit, s, nm);
+        case 20: return launch_ftc64<16, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
+        case 21: return launch_ftc64<20, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
+        case 22: return launch_ftc64<20, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
+        case 23: return launch_ftc64<16, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
