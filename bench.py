@@ -437,7 +437,7 @@ def device_rank(args, spec, batch, ctx, units) -> dict:
         if not args.tuned_from and not args.no_autotune:
             tuned = graphs[0].autotune(x_dev)
             if args.tuned_out:
-                Path(args.tuned_out).write_text(json.dumps(graphs[0].tuning()))
+                Path(args.tuned_out).write_text(json.dumps(graphs[0].tuning_names()))
         for g in graphs[1:]:  # same architecture (sweep candidates): same shapes -> same picks
             if tuned:
                 g.copy_tuning(graphs[0])

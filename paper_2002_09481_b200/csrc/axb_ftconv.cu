@@ -48,10 +48,12 @@ constexpr int kFtSubPairs = 4;                     // channel pairs per 8-channe
 constexpr int kFtRowWords = kFtSubPairs * 256;     // one (sub-block, row) slice: 4 pairs x 256 codes
 constexpr int kFtRowBytes = kFtRowWords * 4;       // 4 KiB
 
+// per-warp epilogue constants of a tile's BN = 2*NPB channels: int64 correction term + fp32 bias (16 warps max)
+__host__ __device__ constexpr int ft_epi_bytes(int NPB) { return 16 * 2 * NPB * 12; }
 // NPB = channel pairs per tile (4: 8 channels, 8: 16 channels); a stage holds KS rows
 __host__ __device__ constexpr int ft_stage_bytes(int NPB, int KS) { return (NPB / 4) * KS * kFtRowBytes; }
 __host__ __device__ constexpr int ft_smem(int NPB, int KS, int ST) {
-    return ST * ft_stage_bytes(NPB, KS) + kMaxTaps * 4 + 2 * ST * 8;
+    return ST * ft_stage_bytes(NPB, KS) + kMaxTaps * 4 + 2 * ST * 8 + ft_epi_bytes(NPB);
 }
 
 // CL > 1: a thread-block cluster of CL CTAs works on CL pixel tiles of the SAME channel block in
@@ -75,6 +77,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
     int32_t *tapoff_s = reinterpret_cast<int32_t *>(smem + ST * STAGE_BYTES);
     uint64_t *full = reinterpret_cast<uint64_t *>(tapoff_s + kMaxTaps);
     uint64_t *empty = full + ST;
+    static_assert(WARPS <= 16, "per-warp epilogue constants");
+    int64_t *epi_cc = reinterpret_cast<int64_t *>(empty + ST) + (threadIdx.x >> 5) * BN;  // this warp's
+    float *epi_bv = reinterpret_cast<float *>(reinterpret_cast<int64_t *>(empty + ST) + 16 * BN) + (threadIdx.x >> 5) * BN;
     const uint32_t *tab = reinterpret_cast<const uint32_t *>(smem);
 
     const int tid = (int)threadIdx.x;
@@ -276,6 +281,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
             const int64_t m0 = ((c_tile % p.ntm) * CL + rank) * BM;
             const int cb = (int)nb * BN;
             const bool full_blk = cb + BN <= p.cout && (p.cout & 3) == 0;
+            const bool has_res = p.residual != nullptr, relu = p.relu != 0;
+            // the tile's per-channel terms, computed once per warp into shared memory and read back as
+            // broadcasts: -zp1*S_f + K*zp1*zp2 - (entry bias), and the bias (-0.0f when absent: x + -0 == x)
+            __syncwarp();
+            if (lane < BN) {
+                const bool ok = cb + lane < p.cout;
+                epi_cc[lane] = ok ? e.kzz - e.zp1 * __ldg(p.fsum + cb + lane) - bias_units : 0;
+                epi_bv[lane] = (ok && p.bias) ? __ldg(p.bias + cb + lane) : -0.0f;
+            }
+            __syncwarp();
 #pragma unroll
             for (int i = 0; i < TM; ++i) {
                 const int64_t mt = m0 + warp * 32 * TM + i * 32 + lane;
@@ -287,52 +302,53 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
                     // four channels (two packed pairs) at a time: float4 stores, few live registers
 #pragma unroll
                     for (int q = 0; q < NPB / 2; ++q) {
-                        int64_t A[4];
+                        // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254); fp64 dequant (:256);
+                        // bias (graph.py:268-269), Add (:282-286), ReLU (:276-277)
+                        float y[4];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const uint32_t hi = acc_hi[i][2 * q + h];
                             const uint32_t lo = acc_all[i][2 * q + h] - (hi << 16);
-                            A[2 * h] = (int64_t)lo - bias_units;
-                            A[2 * h + 1] = (int64_t)hi - bias_units;
+                            const int c = 4 * q + 2 * h;
+                            y[2 * h] = __fadd_rn(
+                                __double2float_rn(e.scale * __ll2double_rn((int64_t)lo + (pz + epi_cc[c]))), epi_bv[c]);
+                            y[2 * h + 1] = __fadd_rn(
+                                __double2float_rn(e.scale * __ll2double_rn((int64_t)hi + (pz + epi_cc[c + 1]))),
+                                epi_bv[c + 1]);
                         }
                         const int c0 = cb + 4 * q;
                         if (full_blk) {
-                            float y[4];
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254); fp64 dequant (:256)
-                                const int64_t corr = A[j] + pz - e.zp1 * __ldg(p.fsum + c0 + j) + e.kzz;
-                                y[j] = __double2float_rn(e.scale * __ll2double_rn(corr));
-                                if (p.bias) y[j] = __fadd_rn(y[j], __ldg(p.bias + c0 + j));  // graph.py:268-269
-                            }
-                            if (p.residual) {  // graph.py:282-286
+                            if (has_res) {
                                 const float4 r = __ldg(reinterpret_cast<const float4 *>(p.residual + m * p.cout + c0));
                                 y[0] = __fadd_rn(y[0], r.x); y[1] = __fadd_rn(y[1], r.y);
                                 y[2] = __fadd_rn(y[2], r.z); y[3] = __fadd_rn(y[3], r.w);
                             }
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                if (p.relu) y[j] = (y[j] > 0.0f || y[j] != y[j]) ? y[j] : 0.0f;  // np.maximum(x, 0)
+                                if (relu) y[j] = (y[j] > 0.0f || y[j] != y[j]) ? y[j] : 0.0f;  // np.maximum(x, 0)
                                 track(y[j], tmin, tmax, nonfinite);
                             }
                             *reinterpret_cast<float4 *>(dst + 4 * q) = make_float4(y[0], y[1], y[2], y[3]);
-                            if (p.acc_out) {
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) p.acc_out[m * p.cout + c0 + j] = A[j];
-                            }
                         } else {
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
                                 if (c0 + j < p.cout) {
-                                    const int64_t corr = A[j] + pz - e.zp1 * p.fsum[c0 + j] + e.kzz;
-                                    float v = __double2float_rn(e.scale * __ll2double_rn(corr));
-                                    if (p.bias) v = __fadd_rn(v, p.bias[c0 + j]);
-                                    if (p.residual) v = __fadd_rn(v, p.residual[m * p.cout + c0 + j]);
-                                    if (p.relu) v = (v > 0.0f || v != v) ? v : 0.0f;
+                                    float v = y[j];
+                                    if (has_res) v = __fadd_rn(v, p.residual[m * p.cout + c0 + j]);
+                                    if (relu) v = (v > 0.0f || v != v) ? v : 0.0f;
                                     track(v, tmin, tmax, nonfinite);
                                     dst[4 * q + j] = v;
-                                    if (p.acc_out) p.acc_out[m * p.cout + c0 + j] = A[j];
                                 }
+                            }
+                        }
+                        if (p.acc_out) {
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const uint32_t hi = acc_hi[i][2 * q + h];
+                                const uint32_t lo = acc_all[i][2 * q + h] - (hi << 16);
+                                const int c = c0 + 2 * h;
+                                if (c < p.cout) p.acc_out[m * p.cout + c] = (int64_t)lo - bias_units;
+                                if (c + 1 < p.cout) p.acc_out[m * p.cout + c + 1] = (int64_t)hi - bias_units;
                             }
                         }
                     }
@@ -1132,15 +1148,11 @@ static const FtVariant kFtVariants[] = {
     {"cm32_j8_w8_k4", 8, 8, 16, 1, 1.000f, 1},
     {"cm32_j4_w12_k4", 4, 12, 16, 1, 1.000f, 1},
     {"cm32_j6_w16_k4", 6, 16, 16, 1, 1.000f, 1},
-    {"c64_j8_w16_k2", 8, 16, 32, 1, 1.000f, 2},
     {"c64_j8_w12_k2", 8, 12, 32, 1, 1.000f, 2},
-    {"c64_j8_w8_k2", 8, 8, 32, 1, 1.000f, 2},
-    {"c64_j8_w16_k1", 8, 16, 32, 1, 1.000f, 2},
     {"c64_j16_w8_k2", 16, 8, 32, 1, 1.000f, 2},
     {"c64_j16_w8_k2_pw", 16, 8, 32, 1, 1.000f, 2},
-    {"c64_j20_w8_k2_pw", 20, 8, 32, 1, 1.000f, 2},
-    {"c64_j20_w8_k2_pw_c4", 20, 8, 32, 1, 1.000f, 2},
     {"c64_j16_w8_k2_pw_c4", 16, 8, 32, 1, 1.000f, 2},
+    {"c64_j20_w8_k2_pw_c4", 20, 8, 32, 1, 1.000f, 2},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
@@ -1358,15 +1370,11 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 12: return launch_ftcm<8, 8, SGN>(op, k, sm_limit, s, nm);
         case 13: return launch_ftcm<4, 12, SGN>(op, k, sm_limit, s, nm);
         case 14: return launch_ftcm<6, 16, SGN>(op, k, sm_limit, s, nm);
-        case 15: return launch_ftc64<8, 16, SGN>(op, k, sm_limit, s, nm);
-        case 16: return launch_ftc64<8, 12, SGN>(op, k, sm_limit, s, nm);
-        case 17: return launch_ftc64<8, 8, SGN>(op, k, sm_limit, s, nm);
-        case 18: return launch_ftc64<8, 16, SGN, 1, 6>(op, k, sm_limit, s, nm);
-        case 19: return launch_ftc64<16, 8, SGN, 2, 3, 8>(op, k, sm_limit, s, nm);
-        case 20: return launch_ftc64<16, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
-        case 21: return launch_ftc64<20, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
-        case 22: return launch_ftc64<20, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
-        case 23: return launch_ftc64<16, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
+        case 15: return launch_ftc64<8, 12, SGN>(op, k, sm_limit, s, nm);
+        case 16: return launch_ftc64<16, 8, SGN, 2, 3, 8>(op, k, sm_limit, s, nm);
+        case 17: return launch_ftc64<16, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
+        case 18: return launch_ftc64<16, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
+        case 19: return launch_ftc64<20, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }

@@ -465,10 +465,15 @@ class GpuGraph:
         """{conv node id: kernel choice} (ftable variant index; 0 = cost model, -1 = b-major LUT kernel)."""
         return {st.node["id"]: st.plan.ft_variant for st in self.steps if st.kind == "conv"}
 
+    def tuning_names(self) -> dict:
+        """tuning() with variant names instead of indices (stable across library builds; --tuned-out files)."""
+        return {k: variant_name(v) for k, v in self.tuning().items()}
+
     def set_tuning(self, picks: dict) -> None:
+        """Adopt per-layer kernel choices: variant indices (tuning()) or names (tuning_names())."""
         for st in self.steps:
             if st.kind == "conv" and st.node["id"] in picks:
-                st.plan.ft_variant = int(picks[st.node["id"]])
+                st.plan.ft_variant = variant_index(picks[st.node["id"]])
                 if st.plan.layer is not None:
                     st.plan.layer.keep_tables(st.plan.ft_variant)
 
@@ -660,6 +665,21 @@ def variant_name(v: int) -> str:
     if v < 0:
         return "lut_bmajor"
     return _lib.load().axb_ft_variant_name(int(v)).decode() if v else "auto"
+
+
+def variant_index(v) -> int:
+    """Inverse of variant_name (ints pass through)."""
+    if not isinstance(v, str):
+        return int(v)
+    if v == "lut_bmajor":
+        return -1
+    if v == "auto":
+        return 0
+    lib = _lib.load()
+    for i in range(1, lib.axb_ft_variant_count()):
+        if lib.axb_ft_variant_name(i).decode() == v:
+            return i
+    raise ValueError(f"unknown kernel variant {v!r}")
 
 
 def run(nodes, batch, **kw) -> torch.Tensor:

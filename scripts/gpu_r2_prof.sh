@@ -12,9 +12,9 @@ for NV in ${LAYERS:-s0b1.b:c64_j16_w8_k2 s1b1.c:c64_j16_w8_k2}; do
 done
 if [ -n "$STEP" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r50_$T.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --tuned-from ${TUNED:-gpurun_out/tuned_r50_s3.json} > /dev/null 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --tuned-from ${TUNED:-profiles/r2_tuned_r50.json} > /dev/null 2>&1
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:lutconv -c 54 \
     --csv --log-file gpurun_out/traffic_r50_$T.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
-    --tuned-from ${TUNED:-gpurun_out/tuned_r50_s3.json} > /dev/null 2>&1
+    --tuned-from ${TUNED:-profiles/r2_tuned_r50.json} > /dev/null 2>&1
 fi
 du -sh gpurun_out
