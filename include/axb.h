@@ -191,8 +191,16 @@ int axb_ftable_cm_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64
 int64_t axb_ftable_c64_bytes(int64_t kpad, int64_t coutp);
 int axb_ftable_c64_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
                            const axb_lut *lut, uint32_t *d_ftable, void *stream);
+/* CX layouts (c64_* / c32_* / c16_* variants, axb_ft_variant_layout(v) == 2 / 3 / 4): channel blocks of
+ * cb = 64 / 32 / 16, every (block, row, code) a 128-byte row holding the block's cb/2 pair words
+ * repeated 64/cb times (cb = 64: exactly the C64 layout above).  A pixel's cb/8 lanes read the copy no
+ * other pixel of their quarter-warp reads: conflict-free at every channel width.
+ * axb_ftable_cx_bytes = kpad * (coutp / cb) * 32768 (0 unless coutp % cb == 0). */
+int64_t axb_ftable_cx_bytes(int64_t kpad, int64_t coutp, int cb);
+int axb_ftable_cx_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                          const axb_lut *lut, uint32_t *d_ftable, void *stream, int cb);
 /* 0: variant v reads the pair-major table (axb_ftable_prepare), 1: the 32-channel code-major one,
- * 2: the 64-channel code-major one */
+ * 2 / 3 / 4: the CX table with 64 / 32 / 16-channel blocks */
 int axb_ft_variant_layout(int variant);
 int axb_conv_variant_count(void);
 /* Depthwise approximate conv (config 5; the reference has no groups): channel c

@@ -643,38 +643,47 @@ constexpr int kC64Pairs = 32;                   // channel pairs per 64-channel 
 constexpr int kC64RowWords = 256 * kC64Pairs;   // one (block, row) slice: 256 codes x 32 pairs
 constexpr int kC64RowBytes = kC64RowWords * 4;  // 32 KiB
 __host__ __device__ constexpr int c64_stage_bytes(int KS) { return KS * kC64RowBytes; }
-__host__ __device__ constexpr int c64_codebuf_bytes(int WARPS, int J) { return WARPS * 2 * 4 * J * 16; }
-__host__ __device__ constexpr int c64_smem(int KS, int ST, int WARPS, int J) {
-    return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS, J) + kMaxTaps * 4 + 2 * ST * 8 + 16;
+// CB < 64 (the CX layouts): a code's CB channels (2*CB bytes) are stored 64/CB times side by side, so the
+// row is still 128 bytes; a pixel takes CB/8 lanes and the copy (pixel slot % copies) no other pixel of
+// its quarter-warp reads -- conflict-free for any codes at every channel width.  Pixels per warp
+// instruction PPI = 256 / CB.
+__host__ __device__ constexpr int cx_ppi(int CB) { return 256 / CB; }
+__host__ __device__ constexpr int c64_codebuf_bytes(int WARPS, int J, int CB = 64) { return WARPS * 2 * cx_ppi(CB) * J * 16; }
+__host__ __device__ constexpr int c64_smem(int KS, int ST, int WARPS, int J, int CB = 64) {
+    return ST * c64_stage_bytes(KS) + c64_codebuf_bytes(WARPS, J, CB) + kMaxTaps * 4 + 2 * ST * 8 + 16;
 }
 // tail-split workspace: 32-bit words per thread for one piece's partial sums (acc_all, acc_hi, S_p)
-__host__ __device__ constexpr int c64_split_words(int J) { return 8 * J + (4 * J + 31) / 32; }
+__host__ __device__ constexpr int c64_split_words(int J, int CB = 64) { return 8 * J + (cx_ppi(CB) * J + 31) / 32; }
 
 // PW = 1: an extra warpgroup whose first thread is the TMA producer (it refills a slot the moment the
 // last consumer warp released it); it gives its registers to the consumers (setmaxnreg).  PW = 0: thread 0
 // refills the previous stage's slot at the start of each stage.
-template <int J, int WARPS, int KS, int ST, bool SGN, int CR, int PW>
+template <int J, int WARPS, int KS, int ST, bool SGN, int CR, int PW, int CB>
 __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_ftc64(const ConvK p) {
     constexpr int NT = WARPS * 32;  // consumer threads
-    constexpr int PXW = 4 * J;        // pixels per warp
+    constexpr int LPP = CB / 8;       // lanes per pixel (8 channels = 4 pairs each)
+    constexpr int PPI = cx_ppi(CB);   // pixels per warp instruction
+    constexpr int RCP = 64 / CB;      // copies of a code's channels in its 128-byte row
+    constexpr int PXW = PPI * J;      // pixels per warp
     constexpr int NPL = (PXW + 31) / 32;  // pixels whose codes each lane stages (the last slot may be partial)
     constexpr int BM = WARPS * PXW;
-    constexpr int BN = 64;
+    constexpr int BN = CB;
     constexpr int SPG = CR / KS;      // stages per CR-row code group
     constexpr int NG = 16 / CR;       // code groups per 16-row chunk
     constexpr int SPCH = 16 / KS;     // stages per 16-row chunk
     constexpr int CBW = PXW * 16;     // one of a warp's two code buffers (bytes)
-    constexpr int WPT = c64_split_words(J);
+    constexpr int WPT = c64_split_words(J, CB);
+    static_assert(CB == 16 || CB == 32 || CB == 64, "channel block of 16, 32 or 64");
     constexpr uint32_t STAGE_BYTES = c64_stage_bytes(KS);
     static_assert(PXW % 16 == 0, "whole 16-pixel groups per warp (J = 8, 12, 16, 20, ...)");
     static_assert(CR == 4 || CR == 8, "code rows per register load: 4 (LDS.32) or 8 (LDS.64)");
     static_assert(KS == 1 || KS == 2 || KS == 4, "KS rows per stage: 1, 2 or 4");
     static_assert(CR % KS == 0, "a stage never straddles two code groups");
-    static_assert(c64_smem(KS, ST, WARPS, J) + 512 <= 232448, "C64 ring exceeds shared memory");
+    static_assert(c64_smem(KS, ST, WARPS, J, CB) + 512 <= 232448, "C64 ring exceeds shared memory");
 
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *codebuf = smem + ST * STAGE_BYTES;  // [warp][2][PXW pixels][16 B]
-    int32_t *tapoff_s = reinterpret_cast<int32_t *>(codebuf + c64_codebuf_bytes(WARPS, J));
+    int32_t *tapoff_s = reinterpret_cast<int32_t *>(codebuf + c64_codebuf_bytes(WARPS, J, CB));
     uint64_t *full = reinterpret_cast<uint64_t *>(tapoff_s + kMaxTaps);
     uint64_t *empty = full + ST;
     int32_t *last_s = reinterpret_cast<int32_t *>(empty + ST);  // tail split: "this CTA reduces the tile"
@@ -682,7 +691,7 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_ftc64(const 
     const int tid = (int)threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int o = lane & 7, ps = lane >> 3;
+    const int o = lane % LPP, ps = lane / LPP;  // channel octet, pixel slot of the warp instruction
 
     if (tid == 0) {
         for (int s = 0; s < ST; ++s) {
@@ -823,7 +832,7 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_ftc64(const 
         ld_item();
         load_next();
     }
-    const uint8_t *tab_lane = smem + o * 16;
+    const uint8_t *tab_lane = smem + (ps % RCP) * (2 * CB) + o * 16;
     for (int kk = 0; kk < n_items; ++kk) {
         int c_tile, kcb, kce, pc;
         item(kk, c_tile, kcb, kce, pc);
@@ -855,7 +864,7 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_ftc64(const 
                 uint32_t cur[J][CR / 4];
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
-                    const uint8_t *src = cb_ + (j * 4 + ps) * 16 + gr * CR;
+                    const uint8_t *src = cb_ + (j * PPI + ps) * 16 + gr * CR;
                     if (CR == 8) {
                         const uint2 v = *reinterpret_cast<const uint2 *>(src);
                         cur[j][0] = v.x;
@@ -976,8 +985,8 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_ftc64(const 
             }
 #pragma unroll
             for (int j = 0; j < J; ++j) {
-                const int32_t spj = __shfl_sync(0xffffffffu, spl[j >> 3], (j * 4 + ps) & 31);
-                const int64_t mt = m0 + warp * PXW + j * 4 + ps;
+                const int32_t spj = __shfl_sync(0xffffffffu, spl[(j * PPI) >> 5], (j * PPI + ps) & 31);
+                const int64_t mt = m0 + warp * PXW + j * PPI + ps;
                 if (mt < p.M) {
                     int64_t pix0;
                     const int64_t m = pixel_of(p, mt, pix0);
@@ -1099,22 +1108,23 @@ __global__ void ftable_cm_kernel(const uint8_t *__restrict__ fcodes, int64_t kpa
     }
 }
 
-// C64[cb][k][a][pr] = W word of channels (cb*64 + 2*pr, +1) at row k, code a (128 B per code and row)
+// CX[blk][k][a][w] (w = 0..31 words, 128 B per code and row) = W word of channels (blk*CB + 2*pr, +1),
+// pr = w % (CB/2): the CB channels of the block, repeated 64/CB times across the row (CB = 64: C64)
 __global__ void ftable_c64_kernel(const uint8_t *__restrict__ fcodes, int64_t kpad, int64_t coutp, int32_t cs,
                                   int32_t c, int64_t kreal, const uint16_t *__restrict__ lut_b, int sgn,
-                                  uint32_t *__restrict__ out) {
-    const int64_t total = (coutp / 64) * kpad * kC64RowWords;
+                                  uint32_t *__restrict__ out, int32_t CB) {
+    const int64_t total = (coutp / CB) * kpad * kC64RowWords;
     const uint32_t flip = sgn ? 0x8000u : 0u;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
-        const int pr = (int)(idx & 31);
+        const int pr = (int)(idx & 31) % (CB / 2);
         const uint32_t a = (uint32_t)((idx >> 5) & 255);
         const int64_t rest = idx >> 13;
         const int64_t k = rest % kpad;
         const int64_t cb = rest / kpad;
         uint32_t w = flip | (flip << 16);
         if (k < kreal && (int)(k % cs) < c) {
-            const int64_t col = cb * 64 + 2 * pr;
+            const int64_t col = cb * CB + 2 * pr;
             const uint32_t b0 = fcodes[k * coutp + col], b1 = fcodes[k * coutp + col + 1];
             const uint32_t u0 = (uint32_t)__ldg(lut_b + b0 * 256 + a) ^ flip;
             const uint32_t u1 = (uint32_t)__ldg(lut_b + b1 * 256 + a) ^ flip;
@@ -1130,7 +1140,7 @@ struct FtVariant {
     int tm, warps, npb, cl;
     float cost;  // relative time per lookup slot (1 = best); tuned on B200
     int cm;      // 1: code-major 32-channel table (axb_ftable_cm_prepare), tm = J pixels per lane per 8-pixel
-                 // group; 2: code-major 64-channel table (axb_ftable_c64_prepare), tm = J pixels per lane
+                 // group; 2 / 3 / 4: CX table of 64 / 32 / 16-channel blocks (axb_ftable_cx_prepare), tm = J
 };
 static const FtVariant kFtVariants[] = {
     {"auto", 0, 0, 0, 0, 0.f},
@@ -1153,6 +1163,11 @@ static const FtVariant kFtVariants[] = {
     {"c64_j16_w8_k2_pw", 16, 8, 32, 1, 1.000f, 2},
     {"c64_j16_w8_k2_pw_c4", 16, 8, 32, 1, 1.000f, 2},
     {"c64_j20_w8_k2_pw_c4", 20, 8, 32, 1, 1.000f, 2},
+    {"c32_j16_w8_k2_pw_c4", 16, 8, 16, 1, 1.000f, 3},
+    {"c32_j8_w8_k2_pw_c4", 8, 8, 16, 1, 1.000f, 3},
+    {"c16_j16_w8_k2_s2_pw_c4", 16, 8, 8, 1, 1.000f, 4},
+    {"c16_j16_w8_k1_s4_pw_c4", 16, 8, 8, 1, 1.000f, 4},
+    {"c16_j8_w8_k2_pw_c4", 8, 8, 8, 1, 1.000f, 4},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
@@ -1239,12 +1254,12 @@ static bool c64_split_enabled() {
     return on != 0;
 }
 
-template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3, int CR = 8, int PW = 0>
+template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3, int CR = 8, int PW = 0, int CB = 64>
 static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
-    constexpr int BM = WARPS * 4 * J;
-    constexpr int BN = 64;
-    const size_t smem = c64_smem(KS, ST, WARPS, J);
-    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN, CR, PW>;
+    constexpr int BM = WARPS * cx_ppi(CB) * J;
+    constexpr int BN = CB;
+    const size_t smem = c64_smem(KS, ST, WARPS, J, CB);
+    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN, CR, PW, CB>;
     static int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1254,7 +1269,7 @@ static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, co
         configured_dev = dev;
     }
     if (op == 1) return sm_count();
-    if (k.coutp % BN) return set_error(AXB_E_VALUE, "64-channel code-major kernel needs coutp % 64 == 0");
+    if (k.coutp % BN) return set_error(AXB_E_VALUE, "code-major kernel needs coutp % its channel block == 0");
     ConvK kk = k;
     kk.ntm = (int32_t)((k.M + BM - 1) / BM);
     kk.ntiles = (int64_t)kk.ntm * (k.coutp / BN);
@@ -1271,7 +1286,7 @@ static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, co
     void *ws = nullptr;
     if (split_s > 1) {
         keep_pool_memory(dev);
-        const size_t ws_bytes = (size_t)split_L * split_s * (WARPS * 32) * c64_split_words(J) * 4;
+        const size_t ws_bytes = (size_t)split_L * split_s * (WARPS * 32) * c64_split_words(J, CB) * 4;
         const size_t cnt_bytes = (size_t)split_L * 4;
         if (cudaMallocAsync(&ws, ws_bytes + cnt_bytes, s) != cudaSuccess)
             return set_error(AXB_E_CUDA, "cannot allocate the c64 tail-split workspace");
@@ -1375,6 +1390,11 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 17: return launch_ftc64<16, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
         case 18: return launch_ftc64<16, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
         case 19: return launch_ftc64<20, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
+        case 20: return launch_ftc64<16, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
+        case 21: return launch_ftc64<8, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
+        case 22: return launch_ftc64<16, 8, SGN, 2, 2, 4, 1, 16>(op, k, sm_limit, s, nm);
+        case 23: return launch_ftc64<16, 8, SGN, 1, 4, 4, 1, 16>(op, k, sm_limit, s, nm);
+        case 24: return launch_ftc64<8, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
@@ -1457,26 +1477,33 @@ int axb_ftable_cm_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64
     return check_launch("ftable_cm_prepare");
 }
 
-int64_t axb_ftable_c64_bytes(int64_t kpad, int64_t coutp) {
-    if (kpad <= 0 || coutp <= 0 || kpad % 16 || coutp % 64) return 0;
-    return kpad * (coutp / 64) * kC64RowBytes;
+int64_t axb_ftable_cx_bytes(int64_t kpad, int64_t coutp, int cb) {
+    if (kpad <= 0 || coutp <= 0 || kpad % 16 || (cb != 16 && cb != 32 && cb != 64) || coutp % cb) return 0;
+    return kpad * (coutp / cb) * kC64RowBytes;
 }
+int64_t axb_ftable_c64_bytes(int64_t kpad, int64_t coutp) { return axb_ftable_cx_bytes(kpad, coutp, 64); }
 
 int axb_ftable_c64_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
                            const axb_lut *lut, uint32_t *d_ftable, void *stream) {
+    return axb_ftable_cx_prepare(d_fcodes, kh, kw, c, cs, cout, lut, d_ftable, stream, 64);
+}
+
+int axb_ftable_cx_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64_t c, int64_t cs, int64_t cout,
+                          const axb_lut *lut, uint32_t *d_ftable, void *stream, int cb) {
     if (!lut || !d_fcodes || !d_ftable) return set_error(AXB_E_VALUE, "null argument");
     if (cs % 16 || c > cs || c < 1) return set_error(AXB_E_VALUE, "channel stride mismatch");
+    if (cb != 16 && cb != 32 && cb != 64) return set_error(AXB_E_VALUE, "channel block must be 16, 32 or 64");
     const int64_t kpad = axb_filter_kpad(kh, kw, cs), coutp = axb_filter_coutp(cout);
-    if (coutp % 64) return set_error(AXB_E_VALUE, "64-channel code-major table needs coutp % 64 == 0");
-    const int64_t total = (coutp / 64) * kpad * kC64RowWords;
+    if (coutp % cb) return set_error(AXB_E_VALUE, "code-major table needs coutp % channel block == 0");
+    const int64_t total = (coutp / cb) * kpad * kC64RowWords;
     int64_t blocks = (total + 255) / 256;
     const int64_t cap = (int64_t)sm_count() * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     ftable_c64_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(d_fcodes, kpad, coutp, (int32_t)cs, (int32_t)c,
                                                                       kh * kw * cs, lut->d_bmajor, lut->is_signed,
-                                                                      d_ftable);
-    return check_launch("ftable_c64_prepare");
+                                                                      d_ftable, (int32_t)cb);
+    return check_launch("ftable_cx_prepare");
 }
 
 int axb_ft_variant_layout(int v) { return (v >= 1 && v < kNumFtVariants) ? kFtVariants[v].cm : 0; }

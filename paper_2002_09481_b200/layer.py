@@ -29,6 +29,7 @@ from .types import resolve_padding
 
 
 FTABLE_MAX_BYTES = 4 << 30  # per layer (ResNet-50's largest: 4608 x 512 x 512 B = 1.2 GB)
+CX_LAYOUTS = {2: 64, 3: 32, 4: 16}  # axb_ft_variant_layout -> channel block of the CX table
 
 
 class ConvLayer:
@@ -90,11 +91,15 @@ class ConvLayer:
         # each layout is built on first use and ``keep_tables`` frees the one the layer's kernel does not read
         cm_bytes = int(lib.axb_ftable_cm_bytes(self.kpad, self.coutp)) if self.has_ft else 0
         self.cm_ok = bool(cm_bytes and cm_bytes <= FTABLE_MAX_BYTES and os.environ.get("AXB_FTABLE_CM", "1") != "0")
-        # and 64-channel code-major (c64_* variants: bank-conflict-free LDS.128) when channels come in 64s
-        c64_bytes = int(lib.axb_ftable_c64_bytes(self.kpad, self.coutp)) if self.has_ft else 0
-        self.c64_ok = bool(c64_bytes and c64_bytes <= FTABLE_MAX_BYTES
-                           and os.environ.get("AXB_FTABLE_C64", "1") != "0")
-        self.ftable = self.ftable_cm = self.ftable_c64 = self.dwtable = None
+        # and the CX layouts (c64_* / c32_* / c16_* variants: bank-conflict-free LDS.128, 128-byte rows of
+        # 64 / 32 / 16-channel blocks, the narrower ones replicated across the row) when channels divide
+        self.cx_ok = {}
+        for lay, cb in CX_LAYOUTS.items():
+            nb = int(lib.axb_ftable_cx_bytes(self.kpad, self.coutp, cb)) if self.has_ft else 0
+            self.cx_ok[lay] = bool(nb and nb <= FTABLE_MAX_BYTES and os.environ.get("AXB_FTABLE_CX", "1") != "0")
+        self.c64_ok = self.cx_ok[2]
+        self.ftable = self.ftable_cm = self.dwtable = None
+        self.ftable_cx = {}
         if self.has_ft:
             self.pair_table()
         # depthwise: the channel-bank product table (axb_depthwise_table_prepare; conflict-free gathers)
@@ -134,24 +139,31 @@ class ConvLayer:
                                                           torch.cuda.current_stream(self.device).cuda_stream))
         return self.ftable_cm
 
-    def c64_table(self) -> torch.Tensor:
-        """The 64-channel code-major table C64[cb][k][a][pair] (axb_ftable_c64_prepare), built on first use."""
-        if self.ftable_c64 is None:
-            if not self.c64_ok:
-                raise ValueError("c64 ftable variant needs a 64-channel code-major table (coutp % 64 == 0)")
+    def cx_table(self, lay: int = 2) -> torch.Tensor:
+        """The CX table of layout ``lay`` (2 / 3 / 4: 64 / 32 / 16-channel blocks; axb_ftable_cx_prepare),
+        built on first use."""
+        if lay not in self.ftable_cx:
+            cb = CX_LAYOUTS[lay]
+            if not self.cx_ok.get(lay):
+                raise ValueError(f"c{cb} ftable variant needs a {cb}-channel code-major table (coutp % {cb} == 0)")
             fk = self.f_geom
-            self.ftable_c64 = torch.empty(int(self.lib.axb_ftable_c64_bytes(self.kpad, self.coutp)) // 4,
-                                          dtype=torch.int32, device=self.device)
+            t = torch.empty(int(self.lib.axb_ftable_cx_bytes(self.kpad, self.coutp, cb)) // 4, dtype=torch.int32,
+                            device=self.device)
             with torch.cuda.device(self.device):
-                _lib.check(self.lib.axb_ftable_c64_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3],
-                                                           self.cout, self.lut.handle, self.ftable_c64.data_ptr(),
-                                                           torch.cuda.current_stream(self.device).cuda_stream))
-        return self.ftable_c64
+                _lib.check(self.lib.axb_ftable_cx_prepare(self.fcodes.data_ptr(), fk[0], fk[1], fk[2], fk[3],
+                                                          self.cout, self.lut.handle, t.data_ptr(),
+                                                          torch.cuda.current_stream(self.device).cuda_stream, cb))
+            self.ftable_cx[lay] = t
+        return self.ftable_cx[lay]
+
+    def c64_table(self) -> torch.Tensor:
+        """The 64-channel code-major table C64[cb][k][a][pair] (layout 2), built on first use."""
+        return self.cx_table(2)
 
     def layout_ok(self, ft_variant: int) -> bool:
         """Whether this layer can run ftable variant ``ft_variant`` (its table layout fits the channels)."""
         lay = self.lib.axb_ft_variant_layout(int(ft_variant)) if ft_variant > 0 else 0
-        return self.has_ft and (lay == 0 or (lay == 1 and self.cm_ok) or (lay == 2 and self.c64_ok))
+        return self.has_ft and (lay == 0 or (lay == 1 and self.cm_ok) or bool(self.cx_ok.get(lay)))
 
     def keep_tables(self, ft_variant: int) -> None:
         """Free the product-table layouts the chosen kernel does not read (0 / pair-major variants keep
@@ -163,12 +175,11 @@ class ConvLayer:
             self.ftable = None
         if lay != 1:
             self.ftable_cm = None
-        if lay != 2:
-            self.ftable_c64 = None
+        self.ftable_cx = {k: t for k, t in self.ftable_cx.items() if k == lay}
 
     def table_bytes(self) -> int:
         """Device bytes held by this layer's product tables."""
-        return sum(t.numel() * 4 for t in (self.ftable, self.ftable_cm, self.ftable_c64, self.dwtable)
+        return sum(t.numel() * 4 for t in (self.ftable, self.ftable_cm, self.dwtable, *self.ftable_cx.values())
                    if t is not None)
 
     def shares_codes_with(self, other: "ConvLayer") -> bool:
@@ -310,7 +321,7 @@ class ConvLayer:
             table = self.dwtable
         elif self.has_ft and use_ftable:
             lay = lib.axb_ft_variant_layout(int(ft_variant)) if ft_variant else 0
-            table = self.cm_table() if lay == 1 else (self.c64_table() if lay == 2 else self.pair_table())
+            table = self.cm_table() if lay == 1 else (self.cx_table(lay) if lay >= 2 else self.pair_table())
         d.ftable = table.data_ptr() if table is not None else None
         d.ft_variant = int(ft_variant)
         if profile is not None:

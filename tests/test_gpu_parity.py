@@ -97,7 +97,7 @@ def test_all_ftable_variants_bit_identical():
         coutp = -(-case["f"].shape[3] // 16) * 16
         for v in range(1, nvar):
             lay = lib.axb_ft_variant_layout(v)
-            if (lay == 1 and coutp % 32) or (lay == 2 and coutp % 64):  # code-major: 32 / 64-channel blocks
+            if coutp % LAYOUT_BLOCK.get(lay, 16):  # code-major layouts: 32 / 64 / 32 / 16-channel blocks
                 continue
             cm_runs += lay > 0
             y, acc, kern = gpu_conv(case, ft_variant=v)
@@ -887,19 +887,25 @@ def test_projection_reads_first_conv_codes():
     assert gg.launches == 1 + 10 + 10 - 2 + 1  # input range, 10 convs, 10 quantizes minus 2 shared, pool
 
 
-@pytest.mark.parametrize("layout", [1, 2])
+# axb_ft_variant_layout -> channel block of the table the variant reads (0: pair-major, 16-channel tiles)
+LAYOUT_BLOCK = {0: 16, 1: 32, 2: 64, 3: 32, 4: 16}
+
+
+@pytest.mark.parametrize("layout", [1, 2, 3, 4])
 @pytest.mark.parametrize("mode", [O.SIGNED, O.UNSIGNED])
 def test_code_major_variants_vs_oracle(mode, layout):
-    """The code-major kernel families -- cm32_* (32-channel blocks, LDS.128 of 4 pairs, layout 1) and
-    c64_* (64-channel blocks, one pixel per quarter-warp, layout 2) -- over shapes the pair-major test
-    does not reach: cout 32 / 64 / 96 / 128 / 192 (one to three channel blocks, ragged 61 and 150), wide
-    and odd input channels, stride 2, dilation 2, ragged pixel tiles, every accumulator mode, K = 4608."""
+    """The code-major kernel families -- cm32_* (32-channel blocks, LDS.128 of 4 pairs, layout 1) and the
+    CX family c64_* / c32_* / c16_* (64 / 32 / 16-channel blocks in 128-byte rows, one pixel per quarter /
+    eighth / sixteenth of a warp instruction, layouts 2 / 3 / 4) -- over shapes the pair-major test does
+    not reach: cout 16 / 32 / 64 / 96 / 128 / 192 (one to many channel blocks, ragged 61 and 150), wide and
+    odd input channels, stride 2, dilation 2, ragged pixel tiles, every accumulator mode, K = 4608, and
+    tiles cut by the tail split (more CTAs than tiles)."""
     from paper_2002_09481_b200 import _lib
 
     lib = _lib.load()
     cms = [v for v in range(1, lib.axb_ft_variant_count()) if lib.axb_ft_variant_layout(v) == layout]
-    assert len(cms) >= 3
-    blk = 32 if layout == 1 else 64
+    assert len(cms) >= 2
+    blk = LAYOUT_BLOCK[layout]
     rng = np.random.default_rng(4096 + (mode == O.SIGNED))
     shapes = [((3, 9, 13, 16), (3, 3, 16, 32), (1, 1), (1, 1), "same", O.EXACT64),
               ((2, 11, 10, 48), (3, 3, 48, 64), (2, 2), (1, 1), "same", O.WRAP32),
@@ -907,7 +913,9 @@ def test_code_major_variants_vs_oracle(mode, layout):
               ((1, 14, 9, 37), (3, 3, 37, 61), (1, 2), (2, 2), "same", O.EXACT64),
               ((3, 17, 15, 32), (3, 3, 32, 128), (1, 1), (1, 1), "same", O.EXACT64),
               ((2, 9, 9, 80), (1, 1, 80, 150), (2, 2), (1, 1), "valid", O.WRAP32),
-              ((1, 5, 6, 512), (3, 3, 512, 192), (1, 1), (1, 1), "same", O.EXACT64)]
+              ((1, 5, 6, 512), (3, 3, 512, 192), (1, 1), (1, 1), "same", O.EXACT64),
+              ((4, 16, 16, 3), (3, 3, 3, 16), (1, 1), (1, 1), "same", O.EXACT64),
+              ((2, 19, 21, 16), (3, 3, 16, 48), (2, 1), (1, 1), "same", O.EXACT64)]
     for xs, fs, st, dil, pad, acc in shapes:
         if -(-fs[3] // 16) * 16 % blk:
             continue
@@ -920,7 +928,7 @@ def test_code_major_variants_vs_oracle(mode, layout):
         want, want_acc = oracle_conv(case, return_acc=True)
         for v in cms:
             y, acc_got, kern = gpu_conv(case, ft_variant=v)
-            assert kern.startswith("cm32" if layout == 1 else "c64"), kern
+            assert kern.startswith("cm32" if layout == 1 else f"c{blk}"), kern
             assert bits_equal(y, want), (kern, xs, fs)
             assert np.array_equal(acc_got, want_acc), (kern, xs, fs)
 
