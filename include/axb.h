@@ -146,7 +146,9 @@ typedef struct axb_conv_desc {
     int32_t *flags;         /* device int32 flag word                               */
     int32_t force_generic;  /* 1: use the int64 generic kernel (testing)            */
     int32_t sm_limit;       /* 0 = all SMs; else cap persistent grid                 */
-    int32_t variant;        /* fast-kernel tile variant, 0 = heuristic (tuning)      */
+    int32_t variant;        /* fast-kernel tile variant, 0 = heuristic (tuning);     *
+                             * axb_depthwise_lut with a table: 1 = per-pixel kernel  *
+                             * (depthwise_ct) instead of the row-strip one           */
     int32_t pixel_order;    /* lanes -> pixels: 0 auto, 1 row runs, 4 4x8 blocks     */
     const uint32_t *ftable; /* nullable: filter-specialised product table from
                                axb_ftable_prepare; when set (and variant == 0) the

@@ -172,8 +172,8 @@ def kernel_family(variant_name: str) -> str:
         return "lutconv_ft"
     if variant_name.startswith("cm"):
         return "lutconv_ftcm"
-    if variant_name.startswith("c64"):
-        return "lutconv_ftc64"
+    if variant_name.startswith(("c64", "c32", "c16")):
+        return "lutconv_cx"
     if variant_name.startswith("lutconv_"):
         return variant_name
     if variant_name.startswith("depthwise"):

@@ -14,6 +14,8 @@
 // channels of one pixel (coalesced code reads and fp32 stores), the b-major
 // table staged once per persistent CTA by TMA bulk copy.  Bank conflicts are
 // data-dependent (different rows b per lane, bank = (a>>1)&31).
+#include <cstdlib>
+
 #include "axb_convk.cuh"
 
 namespace axb {
@@ -240,9 +242,153 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_ct_kernel(const DwK p) {
                  AXB_FLAG_OUT_NONFINITE);
 }
 
+// ---------------------------------------------------------------- row-strip kernel (3x3, dilation 1)
+// Same channel-bank table and arithmetic as depthwise_ct_kernel, reorganised for memory-level parallelism
+// and reuse: a warp owns a strip of P consecutive output pixels of one row x 32 channels (lane = channel).
+// The strip's 3 x NC input codes (NC = (P-1)*SW + 3 columns, 32 channels each) are copied into the warp's
+// shared buffer with 16-byte cp.async (the next strip's while this one computes: ~1.7 KB in flight per
+// warp instead of one 32-byte load per tap); each code is read once from there, its table address and
+// half-word selector derived once and reused by every tap that reads it (3 for SW = 1); P independent
+// accumulation chains; S_p accumulated per code.
+template <int SW, int P, int NW>
+__host__ __device__ constexpr int dw_rs_strip_bytes() { return 3 * ((P - 1) * SW + 3) * 32; }
+template <int SW, int P, int NW>
+__host__ __device__ constexpr int dw_rs_smem() { return 9 * kDwTapBytes + NW * 2 * dw_rs_strip_bytes<SW, P, NW>() + 16; }
+
+template <int SW, int P, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, FastDiv fd_ns, int32_t nstrips) {
+    constexpr int KH = 3, KW = 3;
+    constexpr int NC = (P - 1) * SW + KW;  // input columns per kernel row
+    constexpr int SB = dw_rs_strip_bytes<SW, P, NW>();
+    constexpr int NCH = 3 * NC * 2;        // 16-byte chunks per strip
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *wbuf = smem + KH * KW * kDwTapBytes + (threadIdx.x >> 5) * 2 * SB;  // this warp's two buffers
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + KH * KW * kDwTapBytes + NW * 2 * SB);
+    const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) mbar_init(bar, 1);
+    __syncthreads();
+
+    const double scale = p.inp->scale * p.fp->scale;
+    const int32_t zp1 = p.inp->zero_point, zp2 = p.fp->zero_point;
+    const int32_t ubias = p.sgn ? 32768 * KH * KW : 0;
+    const int nb = (p.c + 31) / 32;
+    const uint32_t U = (uint32_t)(p.n * p.oh) * (uint32_t)nstrips;  // units per channel block (< 2^31)
+    const int64_t total = (int64_t)nb * U;
+    const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
+    const bool has_res = p.residual != nullptr, relu = p.relu != 0;
+    float tmin = INFINITY, tmax = -INFINITY;
+    int nonfinite = 0;
+    uint32_t phase = 0;
+    const uint8_t *tab_lane = smem + lane * 4;
+    for (int cb = lo < hi ? (int)(lo / U) : nb; cb < nb && (int64_t)cb * U < hi; ++cb) {
+        const uint32_t u0 = (uint32_t)(max(lo, (int64_t)cb * U) - (int64_t)cb * U);
+        const uint32_t u1 = (uint32_t)(min(hi, (int64_t)(cb + 1) * U) - (int64_t)cb * U);
+        // strip u's codes -> buffer `buf`: chunk j = (ky, column i, half h) of 16 channels
+        auto fetch = [&](uint32_t u, int buf) {
+            const uint32_t t1 = fdiv(u, fd_ns);
+            const uint32_t strip = u - t1 * (uint32_t)nstrips;
+            const uint32_t b = fdiv(t1, p.fd_oh);
+            const uint32_t oy = t1 - b * (uint32_t)p.oh;
+            const int col0 = (int)strip * P * SW;
+#pragma unroll
+            for (int j0 = 0; j0 < NCH; j0 += 32) {
+                const int j = j0 + lane;
+                if (j0 + 32 <= NCH || j < NCH) {
+                    const int h = j & 1, i = (j >> 1) % NC, ky = (j >> 1) / NC;
+                    const int col = min(col0 + i, (int)p.wp - 1);  // columns past the row: junk outputs only
+                    const int chan = cb * 32 + h * 16;
+                    const uint8_t *src = p.codes + (((int64_t)b * p.hp + (int64_t)oy * p.sh + ky) * p.wp + col) * p.cs +
+                                         min(chan, (int)p.cs - 16);
+                    cp_async16(wbuf + buf * SB + (ky * NC + i) * 32 + h * 16, src, chan < p.cs ? 16 : 0);
+                }
+            }
+            cp_async_commit();
+        };
+        fence_proxy_async_smem();  // every thread's reads of the previous block's table precede the TMA write
+        __syncthreads();
+        if (tid == 0) {
+            mbar_expect_tx(bar, KH * KW * kDwTapBytes);
+            bulk_g2s(smem, p.dwtable + (int64_t)cb * KH * KW * (kDwTapBytes / 4), KH * KW * kDwTapBytes, bar);
+        }
+        const int ch = cb * 32 + lane;
+        const int chl = min(ch, p.c - 1);
+        // per-channel terms: -zp1*S_f + K*zp1*zp2 - (entry bias); bias (-0.0f when absent: exact identity)
+        const int32_t cc = (int32_t)(KH * KW * zp1 * zp2 - zp1 * (int32_t)p.fsum[chl]) - ubias;
+        const float bias = p.bias ? __ldg(p.bias + chl) : -0.0f;
+        int buf = 0;
+        if (u0 + warp < u1) fetch(u0 + warp, 0);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        for (uint32_t u = u0 + warp; u < u1; u += NW) {
+            if (u + NW < u1) fetch(u + NW, buf ^ 1);
+            else cp_async_commit();
+            cp_async_wait<1>();
+            __syncwarp();
+            const uint32_t t1 = fdiv(u, fd_ns);
+            const uint32_t strip = u - t1 * (uint32_t)nstrips;
+            const uint32_t b = fdiv(t1, p.fd_oh);
+            const uint32_t oy = t1 - b * (uint32_t)p.oh;
+            const int ox0 = (int)strip * P;
+            const uint8_t *cbuf = wbuf + buf * SB + lane;
+            uint32_t A[P];
+            int32_t sp[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) A[q] = 0, sp[q] = 0;
+#pragma unroll
+            for (int ky = 0; ky < KH; ++ky) {
+#pragma unroll
+                for (int i = 0; i < NC; ++i) {
+                    const uint32_t code = cbuf[(ky * NC + i) * 32];
+                    const uint8_t *base = tab_lane + (code >> 1) * 128u + ky * KW * kDwTapBytes;
+                    const uint32_t sel = 0x4410u + (code & 1u) * 0x22u;
+                    const int32_t cv = p.sgn ? (int32_t)(int8_t)code : (int32_t)code;
+#pragma unroll
+                    for (int kx = 0; kx < KW; ++kx) {
+                        const int q = (i - kx) / SW;  // output pixel reading column i at tap kx
+                        if (i - kx >= 0 && (i - kx) % SW == 0 && q < P) {
+                            const uint32_t w = *reinterpret_cast<const uint32_t *>(base + kx * kDwTapBytes);
+                            A[q] += __byte_perm(w, 0, sel);  // the entry of this code (axconv.py:136-146)
+                            sp[q] += cv;
+                        }
+                    }
+                }
+            }
+            __syncwarp();  // every lane read the buffer before the fetch two strips on overwrites it
+            buf ^= 1;
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                if (ch < p.c && ox0 + q < (int)p.ow) {
+                    const int32_t Ai = (int32_t)A[q];  // exact: |A - ubias| <= 9 * 32768
+                    const int64_t o = (((int64_t)b * p.oh + oy) * p.ow + ox0 + q) * p.c + ch;
+                    if (p.acc_out) p.acc_out[o] = Ai - ubias;
+                    // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254), exact in int32 here
+                    const int32_t corr = Ai - zp2 * sp[q] + cc;
+                    float y = __fadd_rn(__double2float_rn(scale * (double)corr), bias);  // :256; graph.py:268-269
+                    if (has_res) y = __fadd_rn(y, __ldg(p.residual + o));               // graph.py:282-286
+                    if (relu) y = (y > 0.0f || y != y) ? y : 0.0f;                      // graph.py:276-277
+                    p.out[o] = y;
+                    track(y, tmin, tmax, nonfinite);
+                }
+            }
+        }
+        cp_async_wait<0>();
+    }
+    const bool any = tmin <= tmax;
+    range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
+                 AXB_FLAG_OUT_NONFINITE);
+}
+
 }  // namespace axb
 
 using namespace axb;
+
+static bool dw_rs_enabled() {
+    static const int on = [] {
+        const char *e = getenv("AXB_DW_RS");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return on != 0;
+}
 
 extern "C" int64_t axb_depthwise_table_bytes(int64_t kh, int64_t kw, int64_t c) {
     if (kh < 1 || kw < 1 || c < 1 || kh * kw > kDwMaxTaps) return 0;
@@ -279,6 +425,35 @@ extern "C" int axb_depthwise_lut(const axb_conv_desc *d, const axb_lut *lut, voi
     k.lut = lut->d_bmajor;
     k.sgn = lut->is_signed;
     k.taps = d->kh * d->kw;
+    if (d->ftable && d->variant != 1 && k.taps == 9 && d->kh == 3 && d->dh == 1 && d->dw == 1 &&
+        (d->sw == 1 || d->sw == 2) &&
+        d->n * d->oh * d->ow < ((int64_t)1 << 31) && dw_rs_enabled()) {
+        // row-strip kernel: strips of 16 (stride 1) / 8 (stride 2) output pixels per warp
+        constexpr int NW = 16, P = 16;
+        k.dwtable = reinterpret_cast<const uint32_t *>(d->ftable);
+        k.fd_oh = make_fastdiv((uint32_t)d->oh);
+        const int ps = d->sw == 1 ? P : P / 2;  // output pixels per strip
+        const int32_t nstrips = (int32_t)((d->ow + ps - 1) / ps);
+        const int64_t units = ((d->c + 31) / 32) * d->n * d->oh * nstrips;
+        if (d->n * d->oh * nstrips >= ((int64_t)1 << 31)) return set_error(AXB_E_VALUE, "depthwise conv too large");
+        const size_t smem = d->sw == 1 ? dw_rs_smem<1, P, NW>() : dw_rs_smem<2, P / 2, NW>();
+        auto fn = d->sw == 1 ? depthwise_rs_kernel<1, P, NW> : depthwise_rs_kernel<2, P / 2, NW>;
+        static int configured[2] = {-1, -1};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int which = d->sw == 1;
+        if (configured[which] != dev) {
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for depthwise_rs_kernel");
+            configured[which] = dev;
+        }
+        int64_t grid = sm_count();
+        if (grid > (units + NW - 1) / NW) grid = (units + NW - 1) / NW;
+        if (grid < 1) grid = 1;
+        fn<<<(int)grid, NW * 32, smem, (cudaStream_t)stream>>>(k, make_fastdiv((uint32_t)nstrips), nstrips);
+        set_last_kernel("depthwise_rs");
+        return check_launch("depthwise_rs");
+    }
     if (d->ftable) {  // channel-bank table kernel (axb_depthwise_table_prepare)
         if (k.taps > kDwMaxTaps) return set_error(AXB_E_VALUE, "depthwise table kernel: more than 13 taps");
         k.dwtable = reinterpret_cast<const uint32_t *>(d->ftable);

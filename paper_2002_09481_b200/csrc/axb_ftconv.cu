@@ -659,7 +659,7 @@ __host__ __device__ constexpr int c64_split_words(int J, int CB = 64) { return 8
 // last consumer warp released it); it gives its registers to the consumers (setmaxnreg).  PW = 0: thread 0
 // refills the previous stage's slot at the start of each stage.
 template <int J, int WARPS, int KS, int ST, bool SGN, int CR, int PW, int CB>
-__global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_ftc64(const ConvK p) {
+__global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_cx(const ConvK p) {
     constexpr int NT = WARPS * 32;  // consumer threads
     constexpr int LPP = CB / 8;       // lanes per pixel (8 channels = 4 pairs each)
     constexpr int PPI = cx_ppi(CB);   // pixels per warp instruction
@@ -1255,17 +1255,17 @@ static bool c64_split_enabled() {
 }
 
 template <int J, int WARPS, bool SGN, int KS = 2, int ST = 3, int CR = 8, int PW = 0, int CB = 64>
-static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
+static int launch_cx(int op, const ConvK &k, int sm_limit, cudaStream_t s, const char *name) {
     constexpr int BM = WARPS * cx_ppi(CB) * J;
     constexpr int BN = CB;
     const size_t smem = c64_smem(KS, ST, WARPS, J, CB);
-    auto fn = lutconv_ftc64<J, WARPS, KS, ST, SGN, CR, PW, CB>;
+    auto fn = lutconv_cx<J, WARPS, KS, ST, SGN, CR, PW, CB>;
     static int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_dev != dev) {
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_ftc64");
+            return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for lutconv_cx");
         configured_dev = dev;
     }
     if (op == 1) return sm_count();
@@ -1309,9 +1309,9 @@ static int launch_ftc64(int op, const ConvK &k, int sm_limit, cudaStream_t s, co
     cfg.numAttrs = ws ? 0 : 1;  // PDL only without the memset in between
     const cudaError_t le = cudaLaunchKernelEx(&cfg, fn, kk);
     if (ws) cudaFreeAsync(ws, s);
-    if (le != cudaSuccess) return check_launch("lutconv_ftc64");
+    if (le != cudaSuccess) return check_launch("lutconv_cx");
     set_last_kernel(name);
-    return check_launch("lutconv_ftc64");
+    return check_launch("lutconv_cx");
 }
 
 // op 0: launch; op 1: return how many CL-CTA clusters fit on the device at once (cached)
@@ -1385,16 +1385,16 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 12: return launch_ftcm<8, 8, SGN>(op, k, sm_limit, s, nm);
         case 13: return launch_ftcm<4, 12, SGN>(op, k, sm_limit, s, nm);
         case 14: return launch_ftcm<6, 16, SGN>(op, k, sm_limit, s, nm);
-        case 15: return launch_ftc64<8, 12, SGN>(op, k, sm_limit, s, nm);
-        case 16: return launch_ftc64<16, 8, SGN, 2, 3, 8>(op, k, sm_limit, s, nm);
-        case 17: return launch_ftc64<16, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
-        case 18: return launch_ftc64<16, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
-        case 19: return launch_ftc64<20, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
-        case 20: return launch_ftc64<16, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
-        case 21: return launch_ftc64<8, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
-        case 22: return launch_ftc64<16, 8, SGN, 2, 2, 4, 1, 16>(op, k, sm_limit, s, nm);
-        case 23: return launch_ftc64<16, 8, SGN, 1, 4, 4, 1, 16>(op, k, sm_limit, s, nm);
-        case 24: return launch_ftc64<8, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);
+        case 15: return launch_cx<8, 12, SGN>(op, k, sm_limit, s, nm);
+        case 16: return launch_cx<16, 8, SGN, 2, 3, 8>(op, k, sm_limit, s, nm);
+        case 17: return launch_cx<16, 8, SGN, 2, 3, 8, 1>(op, k, sm_limit, s, nm);
+        case 18: return launch_cx<16, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
+        case 19: return launch_cx<20, 8, SGN, 2, 3, 4, 1>(op, k, sm_limit, s, nm);
+        case 20: return launch_cx<16, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
+        case 21: return launch_cx<8, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
+        case 22: return launch_cx<16, 8, SGN, 2, 2, 4, 1, 16>(op, k, sm_limit, s, nm);
+        case 23: return launch_cx<16, 8, SGN, 1, 4, 4, 1, 16>(op, k, sm_limit, s, nm);
+        case 24: return launch_cx<8, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }

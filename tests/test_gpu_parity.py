@@ -429,7 +429,8 @@ def test_exact_lut_control_full_size_layer():
 def test_depthwise_matches_per_channel_oracle(stride, shape, mode):
     """Config 5: depthwise approximate conv == per-channel axconv2d with shared ranges (bit-exact), at the
     MobileNet shapes (n,112,112,32) and (n,56,56,128), stride 1 and 2, ragged channel blocks (40, 48):
-    the channel-bank table kernel (depthwise_ct) and the b-major LUT kernel, outputs and raw sums."""
+    the channel-bank table kernels (row-strip depthwise_rs, per-pixel depthwise_ct) and the b-major LUT
+    kernel, outputs and raw sums."""
     torch = _torch()
     from paper_2002_09481_b200.layer import ConvLayer
     from paper_2002_09481_b200.types import ConvGeometry
@@ -451,10 +452,11 @@ def test_depthwise_matches_per_channel_oracle(stride, shape, mode):
                                    return_acc=True)
     from paper_2002_09481_b200 import _lib
 
-    for use_table, kern in ((True, "depthwise_ct"), (False, "depthwise_lut")):
+    for use_table, variant, kern in ((True, 0, "depthwise_rs"), (True, 1, "depthwise_ct"),
+                                     (False, 0, "depthwise_lut")):
         acc = torch.empty(want_acc.shape, dtype=torch.int64, device="cuda")
         y = layer.run(torch.from_numpy(x).cuda(), None, out_flag=flags[0].data_ptr(),
-                      quant_flag=flags[1].data_ptr(), use_ftable=use_table, acc_out=acc)
+                      quant_flag=flags[1].data_ptr(), use_ftable=use_table, acc_out=acc, variant=variant)
         assert _lib.last_kernel() == kern
         assert bits_equal(y.cpu().numpy(), want), kern
         assert np.array_equal(acc.cpu().numpy(), want_acc), kern
@@ -815,10 +817,10 @@ def test_ftable_kernel_long_k_packed_sums_exact(mode):
     want, want_acc = oracle_conv(case, return_acc=True)
     lib = _lib.load()
     for v in range(1, lib.axb_ft_variant_count()):
-        if lib.axb_ft_variant_layout(v) == 2:  # 64-channel blocks: cout 20 pads to 32 (covered below)
+        if 32 % LAYOUT_BLOCK[lib.axb_ft_variant_layout(v)]:  # 64-channel blocks: cout 20 pads to 32
             continue
         y, acc, kern = gpu_conv(case, ft_variant=v)
-        assert kern.startswith(("ft", "cm")), kern
+        assert kern.startswith(("ft", "cm", "c32", "c16")), kern
         assert bits_equal(y, want), kern
         assert np.array_equal(acc, want_acc), kern
 
