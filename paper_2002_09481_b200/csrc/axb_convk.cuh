@@ -89,6 +89,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+// blocking wait that lets the hardware suspend the thread until the phase completes (or ~100 us pass)
+// instead of re-polling: a spinning producer / waiting consumer does not steal issue slots from the
+// warps that share its scheduler
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t phase) {
+#ifdef AXB_NO_SLEEP_WAIT
+    mbar_wait(bar, phase);
+#else
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 100000;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+#endif
+}
 // non-blocking probe: has the phase with this parity completed?
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t phase) {
     uint32_t ok;

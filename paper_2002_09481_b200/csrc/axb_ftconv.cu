@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_cx(const Con
         if (warp == WARPS && lane == 0 && n_items > 0) {
             pr_item();
             for (int h = 0; pr_k < n_items; ++h) {
-                if (h >= ST) mbar_wait(empty + pr_slot, (uint32_t)((h / ST) - 1) & 1u);
+                if (h >= ST) mbar_wait_sleep(empty + pr_slot, (uint32_t)((h / ST) - 1) & 1u);
                 produce();
             }
         }
@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_cx(const Con
                         }
                         produce();
                     }
-                    mbar_wait(full + slot, phase);
+                    mbar_wait_sleep(full + slot, phase);
 #else  // A/B experiment only (wrong products): the first ST-1 stages are loaded once and never refilled
                     if (g < ST - 1) mbar_wait(full + slot, phase);
 #endif
