@@ -1168,6 +1168,8 @@ static const FtVariant kFtVariants[] = {
     {"c16_j16_w8_k2_s2_pw_c4", 16, 8, 8, 1, 1.000f, 4},
     {"c16_j16_w8_k1_s4_pw_c4", 16, 8, 8, 1, 1.000f, 4},
     {"c16_j8_w8_k2_pw_c4", 8, 8, 8, 1, 1.000f, 4},
+    {"c16_j2_w8_k2_pw_c4", 2, 8, 8, 1, 1.000f, 4},
+    {"c32_j4_w8_k2_pw_c4", 4, 8, 16, 1, 1.000f, 3},
 };
 constexpr int kNumFtVariants = sizeof(kFtVariants) / sizeof(kFtVariants[0]);
 
@@ -1395,6 +1397,8 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 22: return launch_cx<16, 8, SGN, 2, 2, 4, 1, 16>(op, k, sm_limit, s, nm);
         case 23: return launch_cx<16, 8, SGN, 1, 4, 4, 1, 16>(op, k, sm_limit, s, nm);
         case 24: return launch_cx<8, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);
+        case 25: return launch_cx<2, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);  // BM = 256: small M (fc)
+        case 26: return launch_cx<4, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);  // BM = 256
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
