@@ -204,6 +204,8 @@ int axb_ftable_cx_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64
 /* 0: variant v reads the pair-major table (axb_ftable_prepare), 1: the 32-channel code-major one,
  * 2 / 3 / 4: the CX table with 64 / 32 / 16-channel blocks */
 int axb_ft_variant_layout(int variant);
+/* largest kpad variant v accepts (CX variants: 8192, their epilogue correction is 32-bit; others 32768) */
+int64_t axb_ft_variant_max_k(int variant);
 int axb_conv_variant_count(void);
 /* Depthwise approximate conv (config 5; the reference has no groups): channel c
  * of the output == axconv2d on input channel c alone with the shared ranges.

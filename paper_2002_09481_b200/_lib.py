@@ -98,6 +98,7 @@ SIGNATURES = {
     "axb_ftable_c64_bytes": (c_i64, [c_i64, c_i64]),
     "axb_ftable_c64_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "axb_ftable_cx_bytes": (c_i64, [c_i64, c_i64, c_int]),
+    "axb_ft_variant_max_k": (c_i64, [c_int]),
     "axb_ftable_cx_prepare": (c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int]),
     "axb_ft_variant_layout": (c_int, [c_int]),
     "axb_depthwise_lut": (c_int, [ctypes.POINTER(ConvDesc), c_vp, c_vp]),

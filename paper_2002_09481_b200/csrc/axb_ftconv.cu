@@ -639,6 +639,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
 // and 64-channel block, read once per BM-pixel tile).  With BM = 384 (J = 8, 12 warps) that is 1.33 B per
 // product -- at ~8.8e12 products/s, 11 TB/s of L2->SM traffic, the chip's L2 read ceiling -- so the tile
 // has to grow: J = 16 at 8 or 10 warps (BM = 512 / 640) cuts it to 1.0 / 0.8 B per product.
+constexpr int kCxMaxK = 8192;  // CX kernels: the 32-bit epilogue correction is exact up to this K
 constexpr int kC64Pairs = 32;                   // channel pairs per 64-channel block
 constexpr int kC64RowWords = 256 * kC64Pairs;   // one (block, row) slice: 256 codes x 32 pairs
 constexpr int kC64RowBytes = kC64RowWords * 4;  // 32 KiB
@@ -973,14 +974,15 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_cx(const Con
             const int cb = nb * BN + o * 8;  // this lane's 8 channels
             const bool full_blk = cb + 8 <= p.cout && (p.cout & 3) == 0;
             const bool has_res = p.residual != nullptr, relu = p.relu != 0;
+
             // per-channel terms hoisted out of the pixel loop: -zp1*S_f + K*zp1*zp2 - (entry bias), and the
             // bias (-0.0f when absent: x + -0 == x for every float, so the add is an exact identity)
-            int64_t cc[8];
+            uint32_t cc[8];  // mod 2^32 (exact in the 32-bit correction below)
             float bv[8];
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const bool ok = full_blk || cb + t < p.cout;
-                cc[t] = ok ? e.kzz - e.zp1 * __ldg(p.fsum + cb + t) - bias_units : 0;
+                cc[t] = ok ? (uint32_t)(e.kzz - e.zp1 * __ldg(p.fsum + cb + t) - bias_units) : 0u;
                 bv[t] = (ok && p.bias) ? __ldg(p.bias + cb + t) : -0.0f;
             }
 #pragma unroll
@@ -994,15 +996,19 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_cx(const Con
                     float *dst = p.out + m * p.cout + cb;
                     // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254), A = sum u - bias_units;
                     // fp64 dequant (:256), bias (graph.py:268-269), Add (:282-286), ReLU (:276-277)
+                    // kpad <= 8192 (the launcher's limit for this kernel): every |corr| < 2^31 (|A| <= 32768 K,
+                    // |zp*S| <= 255*255 K), so the correction is exact in 32-bit two's-complement arithmetic
+                    // whatever the intermediate sums wrap to
                     float y[8];
+                    const uint32_t pz32 = (uint32_t)pz;
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
                         const uint32_t hi = acc_hi[j][h];
                         const uint32_t lo = acc_all[j][h] - (hi << 16);
-                        y[2 * h] = __fadd_rn(__double2float_rn(e.scale * __ll2double_rn((int64_t)lo + (pz + cc[2 * h]))),
-                                             bv[2 * h]);
-                        y[2 * h + 1] = __fadd_rn(
-                            __double2float_rn(e.scale * __ll2double_rn((int64_t)hi + (pz + cc[2 * h + 1]))), bv[2 * h + 1]);
+                        const int32_t c0 = (int32_t)(lo + pz32 + cc[2 * h]);
+                        const int32_t c1 = (int32_t)(hi + pz32 + cc[2 * h + 1]);
+                        y[2 * h] = __fadd_rn(__double2float_rn(e.scale * (double)c0), bv[2 * h]);
+                        y[2 * h + 1] = __fadd_rn(__double2float_rn(e.scale * (double)c1), bv[2 * h + 1]);
                     }
                     if (full_blk) {
                         if (has_res) {
@@ -1051,6 +1057,7 @@ __global__ void __launch_bounds__(WARPS * 32 + PW * 128, 1) lutconv_cx(const Con
     }
     }  // consumers
     cp_async_wait<0>();
+
     const bool any = tmin <= tmax;
     range_commit(any ? f2ord(tmin) : INT32_MAX, any ? f2ord(tmax) : INT32_MIN, nonfinite, p.out_range, p.flags,
                  AXB_FLAG_OUT_NONFINITE);
@@ -1166,7 +1173,6 @@ static const FtVariant kFtVariants[] = {
     {"c32_j16_w8_k2_pw_c4", 16, 8, 16, 1, 1.000f, 3},
     {"c32_j8_w8_k2_pw_c4", 8, 8, 16, 1, 1.000f, 3},
     {"c16_j16_w8_k2_s2_pw_c4", 16, 8, 8, 1, 1.000f, 4},
-    {"c16_j16_w8_k1_s4_pw_c4", 16, 8, 8, 1, 1.000f, 4},
     {"c16_j8_w8_k2_pw_c4", 8, 8, 8, 1, 1.000f, 4},
     {"c16_j2_w8_k2_pw_c4", 2, 8, 8, 1, 1.000f, 4},
     {"c32_j4_w8_k2_pw_c4", 4, 8, 16, 1, 1.000f, 3},
@@ -1272,6 +1278,7 @@ static int launch_cx(int op, const ConvK &k, int sm_limit, cudaStream_t s, const
     }
     if (op == 1) return sm_count();
     if (k.coutp % BN) return set_error(AXB_E_VALUE, "code-major kernel needs coutp % its channel block == 0");
+    if (k.kpad > kCxMaxK) return set_error(AXB_E_VALUE, "CX kernel: K > 8192 (its epilogue corrections are 32-bit)");
     ConvK kk = k;
     kk.ntm = (int32_t)((k.M + BM - 1) / BM);
     kk.ntiles = (int64_t)kk.ntm * (k.coutp / BN);
@@ -1395,10 +1402,9 @@ static int launch_ft_variant(int op, int v, const ConvK &k, int sm_limit, cudaSt
         case 20: return launch_cx<16, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
         case 21: return launch_cx<8, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);
         case 22: return launch_cx<16, 8, SGN, 2, 2, 4, 1, 16>(op, k, sm_limit, s, nm);
-        case 23: return launch_cx<16, 8, SGN, 1, 4, 4, 1, 16>(op, k, sm_limit, s, nm);
-        case 24: return launch_cx<8, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);
-        case 25: return launch_cx<2, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);  // BM = 256: small M (fc)
-        case 26: return launch_cx<4, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);  // BM = 256
+        case 23: return launch_cx<8, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);
+        case 24: return launch_cx<2, 8, SGN, 2, 3, 4, 1, 16>(op, k, sm_limit, s, nm);  // BM = 256: small M (fc)
+        case 25: return launch_cx<4, 8, SGN, 2, 3, 4, 1, 32>(op, k, sm_limit, s, nm);  // BM = 256
         default: return set_error(AXB_E_VALUE, "unknown ftable kernel variant");
     }
 }
@@ -1511,6 +1517,7 @@ int axb_ftable_cx_prepare(const uint8_t *d_fcodes, int64_t kh, int64_t kw, int64
 }
 
 int axb_ft_variant_layout(int v) { return (v >= 1 && v < kNumFtVariants) ? kFtVariants[v].cm : 0; }
+int64_t axb_ft_variant_max_k(int v) { return (v >= 1 && v < kNumFtVariants && kFtVariants[v].cm >= 2) ? kCxMaxK : 32768; }
 
 int axb_ft_variant_count(void) { return kNumFtVariants; }
 int axb_ft_variant_clusters(int v, int is_signed) {

@@ -163,6 +163,8 @@ class ConvLayer:
     def layout_ok(self, ft_variant: int) -> bool:
         """Whether this layer can run ftable variant ``ft_variant`` (its table layout fits the channels)."""
         lay = self.lib.axb_ft_variant_layout(int(ft_variant)) if ft_variant > 0 else 0
+        if ft_variant > 0 and self.kpad > self.lib.axb_ft_variant_max_k(int(ft_variant)):
+            return False
         return self.has_ft and (lay == 0 or (lay == 1 and self.cm_ok) or bool(self.cx_ok.get(lay)))
 
     def keep_tables(self, ft_variant: int) -> None:

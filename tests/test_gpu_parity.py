@@ -816,8 +816,13 @@ def test_ftable_kernel_long_k_packed_sums_exact(mode):
                 f_range=(float(case["f"].min()), float(case["f"].max())))
     want, want_acc = oracle_conv(case, return_acc=True)
     lib = _lib.load()
+    kpad = 3 * 3 * 2048
     for v in range(1, lib.axb_ft_variant_count()):
         if 32 % LAYOUT_BLOCK[lib.axb_ft_variant_layout(v)]:  # 64-channel blocks: cout 20 pads to 32
+            continue
+        if kpad > lib.axb_ft_variant_max_k(v):  # CX variants: 32-bit epilogue, K <= 8192 (layout_ok)
+            with pytest.raises(ValueError, match="K > 8192"):
+                gpu_conv(case, ft_variant=v)
             continue
         y, acc, kern = gpu_conv(case, ft_variant=v)
         assert kern.startswith(("ft", "cm", "c32", "c16")), kern
