@@ -285,6 +285,16 @@ __global__ void __launch_bounds__(256) quantize_pad_kernel(const float *__restri
 // pixel sum is dp4a(u bytes) + 16*lo per chunk (exact).  Any element the fp32
 // estimate cannot decide (near a half-step, NaN/inf) or a toward-zero table
 // sends its whole chunk through the exact path (rare, warp-divergent).
+// round-to-nearest-even of four floats, each clipped to [0, 255] (NaN -> 0), packed little-endian:
+// cvt.pack.sat places sat(a) in bits 15:8, sat(b) in bits 7:0 and c's low half above them (the
+// compiler fuses the float->int rounding into one F2IP.U8 per pair)
+__device__ __forceinline__ uint32_t pack_u8x4(float f0, float f1, float f2, float f3) {
+    uint32_t hi, w;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(__float2int_rn(f3)), "r"(__float2int_rn(f2)));
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(__float2int_rn(f1)), "r"(__float2int_rn(f0)), "r"(hi));
+    return w;
+}
+
 template <int C16>
 __global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__restrict__ x, int n, int h, int w,
                                                              int pt, int pl, int hp, int wp, FastDiv fd_hp,
@@ -341,27 +351,31 @@ __global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__rest
                 out = make_uint4(zpw, zpw, zpw, zpw);
                 s = zsum;
             } else {
-                int u[16];
+                float uf[16];
                 bool ok = nearest;
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
-                    const float uf = fmaf(e[k], inv, zpo);
-                    const float r = rintf(uf);
-                    ok &= fabsf(uf - r) < 0.49975f;  // false near a tie and for NaN / +-inf
-                    u[k] = min(max((int)r, 0), 255);
+                    uf[k] = fmaf(e[k], inv, zpo);
+                    ok &= fabsf(uf[k] - rintf(uf[k])) < 0.49975f;  // false near a tie and for NaN / +-inf
                 }
-                if (__builtin_expect(!ok, 0)) {
+                uint32_t wv[4];
+                if (__builtin_expect(ok, 1)) {
+                    // round to nearest and clip to [0, 255] (quantizer.py:126-130) in the packing
+                    // conversion: two codes per instruction (F2IP.U8)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) wv[v] = pack_u8x4(uf[4 * v], uf[4 * v + 1], uf[4 * v + 2], uf[4 * v + 3]);
+                } else {
+                    int u[16];
 #pragma unroll
                     for (int k = 0; k < 16; ++k) {
                         nonfinite |= !(fabsf(e[k]) <= 3.402823466e38f);
                         u[k] = quant_any_u(q, e[k], nearest);
                     }
-                }
-                uint32_t wv[4];
 #pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    wv[v] = (uint32_t)u[4 * v] | ((uint32_t)u[4 * v + 1] << 8) | ((uint32_t)u[4 * v + 2] << 16) |
-                            ((uint32_t)u[4 * v + 3] << 24);
+                    for (int v = 0; v < 4; ++v)
+                        wv[v] = (uint32_t)u[4 * v] | ((uint32_t)u[4 * v + 1] << 8) | ((uint32_t)u[4 * v + 2] << 16) |
+                                ((uint32_t)u[4 * v + 3] << 24);
+                }
                 uint32_t su = 0;
 #pragma unroll
                 for (int v = 0; v < 4; ++v) su = __dp4a(wv[v], 0x01010101u, su);

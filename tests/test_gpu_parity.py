@@ -675,7 +675,8 @@ def test_graph_autotune_keeps_bits():
     x = torch.from_numpy(imgs).cuda()
     want = g.run(x).cpu().numpy()
     picks = g.autotune(x, reps=1)
-    assert len(picks) == 10 and all(v.startswith(("ft", "cm")) or v == "lut_bmajor" for v in picks.values()), picks
+    assert len(picks) == 10 and all(v.startswith(("ft", "cm", "c16", "c32", "c64")) or v == "lut_bmajor"
+                                    for v in picks.values()), picks
     # only the table layout each layer's pick reads stays resident
     for p in g.conv_plans.values():
         assert p.layer.ftable is None or p.layer.ftable_cm is None, p.node["id"]
