@@ -244,23 +244,28 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_ct_kernel(const DwK p) {
 
 // ---------------------------------------------------------------- row-strip kernel (3x3, dilation 1)
 // Same channel-bank table and arithmetic as depthwise_ct_kernel, reorganised for memory-level parallelism
-// and reuse: a warp owns a strip of P consecutive output pixels of one row x 32 channels (lane = channel).
-// The strip's 3 x NC input codes (NC = (P-1)*SW + 3 columns, 32 channels each) are copied into the warp's
-// shared buffer with 16-byte cp.async (the next strip's while this one computes: ~1.7 KB in flight per
-// warp instead of one 32-byte load per tap); each code is read once from there, its table address and
-// half-word selector derived once and reused by every tap that reads it (3 for SW = 1); P independent
-// accumulation chains; S_p accumulated per code.
-template <int SW, int P, int NW>
-__host__ __device__ constexpr int dw_rs_strip_bytes() { return 3 * ((P - 1) * SW + 3) * 32; }
-template <int SW, int P, int NW>
-__host__ __device__ constexpr int dw_rs_smem() { return 9 * kDwTapBytes + NW * 2 * dw_rs_strip_bytes<SW, P, NW>() + 16; }
+// and reuse: a warp owns R output rows x P consecutive output pixels x 32 channels (lane = channel).  The
+// unit's NR x NC input codes (NR = R + 2 rows at stride 1 -- R = 2 shares two of the three input rows
+// between the two output rows -- NC = (P-1)*SW + 3 columns, 32 channels each) are copied into the
+// warp's shared buffer with 16-byte cp.async, the next unit's while this one computes (~1.3 KB in
+// flight per warp instead of one 32-byte load per tap).  Each code is read once from there; its table
+// address and half-word selector are derived once and reused by every tap of every output row that
+// reads it (up to 6 at stride 1); S_p = sums of per-column code sums.  R * P independent chains.
+template <int SW, int P, int R>
+__host__ __device__ constexpr int dw_rs_nr() { return R + 2; }  // input rows per unit (R > 1: stride 1)
+template <int SW, int P, int R>
+__host__ __device__ constexpr int dw_rs_strip_bytes() { return dw_rs_nr<SW, P, R>() * ((P - 1) * SW + 3) * 32; }
+template <int SW, int P, int R, int NW>
+__host__ __device__ constexpr int dw_rs_smem() { return 9 * kDwTapBytes + NW * 2 * dw_rs_strip_bytes<SW, P, R>() + 16; }
 
-template <int SW, int P, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, FastDiv fd_ns, int32_t nstrips) {
+template <int SW, int P, int R, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, FastDiv fd_ns, int32_t nstrips,
+                                                                  FastDiv fd_ohr, int32_t ohr) {
     constexpr int KH = 3, KW = 3;
     constexpr int NC = (P - 1) * SW + KW;  // input columns per kernel row
-    constexpr int SB = dw_rs_strip_bytes<SW, P, NW>();
-    constexpr int NCH = 3 * NC * 2;        // 16-byte chunks per strip
+    constexpr int NR = dw_rs_nr<SW, P, R>();
+    constexpr int SB = dw_rs_strip_bytes<SW, P, R>();
+    constexpr int NCH = NR * NC * 2;       // 16-byte chunks per unit
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *wbuf = smem + KH * KW * kDwTapBytes + (threadIdx.x >> 5) * 2 * SB;  // this warp's two buffers
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + KH * KW * kDwTapBytes + NW * 2 * SB);
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, F
     const int32_t zp1 = p.inp->zero_point, zp2 = p.fp->zero_point;
     const int32_t ubias = p.sgn ? 32768 * KH * KW : 0;
     const int nb = (p.c + 31) / 32;
-    const uint32_t U = (uint32_t)(p.n * p.oh) * (uint32_t)nstrips;  // units per channel block (< 2^31)
+    const uint32_t U = (uint32_t)(p.n * ohr) * (uint32_t)nstrips;  // units per channel block (< 2^31)
     const int64_t total = (int64_t)nb * U;
     const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
     const bool has_res = p.residual != nullptr, relu = p.relu != 0;
@@ -280,26 +285,32 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, F
     int nonfinite = 0;
     uint32_t phase = 0;
     const uint8_t *tab_lane = smem + lane * 4;
+    // unit u -> image b, first output row oy0, strip
+    auto unit = [&](uint32_t u, uint32_t &b, uint32_t &oy0, uint32_t &strip) {
+        const uint32_t t1 = fdiv(u, fd_ns);
+        strip = u - t1 * (uint32_t)nstrips;
+        b = fdiv(t1, fd_ohr);
+        oy0 = (t1 - b * (uint32_t)ohr) * R;
+    };
     for (int cb = lo < hi ? (int)(lo / U) : nb; cb < nb && (int64_t)cb * U < hi; ++cb) {
         const uint32_t u0 = (uint32_t)(max(lo, (int64_t)cb * U) - (int64_t)cb * U);
         const uint32_t u1 = (uint32_t)(min(hi, (int64_t)(cb + 1) * U) - (int64_t)cb * U);
-        // strip u's codes -> buffer `buf`: chunk j = (ky, column i, half h) of 16 channels
+        // unit u's codes -> buffer `buf`: chunk j = (input row r, column i, half h) of 16 channels
         auto fetch = [&](uint32_t u, int buf) {
-            const uint32_t t1 = fdiv(u, fd_ns);
-            const uint32_t strip = u - t1 * (uint32_t)nstrips;
-            const uint32_t b = fdiv(t1, p.fd_oh);
-            const uint32_t oy = t1 - b * (uint32_t)p.oh;
+            uint32_t b, oy0, strip;
+            unit(u, b, oy0, strip);
             const int col0 = (int)strip * P * SW;
 #pragma unroll
             for (int j0 = 0; j0 < NCH; j0 += 32) {
                 const int j = j0 + lane;
                 if (j0 + 32 <= NCH || j < NCH) {
-                    const int h = j & 1, i = (j >> 1) % NC, ky = (j >> 1) / NC;
+                    const int h = j & 1, i = (j >> 1) % NC, r = (j >> 1) / NC;
                     const int col = min(col0 + i, (int)p.wp - 1);  // columns past the row: junk outputs only
+                    const int row = min((int)oy0 * p.sh + r, (int)p.hp - 1);  // rows past the image: junk too
                     const int chan = cb * 32 + h * 16;
-                    const uint8_t *src = p.codes + (((int64_t)b * p.hp + (int64_t)oy * p.sh + ky) * p.wp + col) * p.cs +
+                    const uint8_t *src = p.codes + (((int64_t)b * p.hp + row) * p.wp + col) * p.cs +
                                          min(chan, (int)p.cs - 16);
-                    cp_async16(wbuf + buf * SB + (ky * NC + i) * 32 + h * 16, src, chan < p.cs ? 16 : 0);
+                    cp_async16(wbuf + buf * SB + (r * NC + i) * 32 + h * 16, src, chan < p.cs ? 16 : 0);
                 }
             }
             cp_async_commit();
@@ -324,50 +335,64 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, F
             else cp_async_commit();
             cp_async_wait<1>();
             __syncwarp();
-            const uint32_t t1 = fdiv(u, fd_ns);
-            const uint32_t strip = u - t1 * (uint32_t)nstrips;
-            const uint32_t b = fdiv(t1, p.fd_oh);
-            const uint32_t oy = t1 - b * (uint32_t)p.oh;
+            uint32_t b, oy0, strip;
+            unit(u, b, oy0, strip);
             const int ox0 = (int)strip * P;
             const uint8_t *cbuf = wbuf + buf * SB + lane;
-            uint32_t A[P];
-            int32_t sp[P];
+            uint32_t A[R][P];
+            int32_t colsum[R][NC];  // per output row and input column: sum of its 3 taps' codes
 #pragma unroll
-            for (int q = 0; q < P; ++q) A[q] = 0, sp[q] = 0;
+            for (int r = 0; r < R; ++r) {
 #pragma unroll
-            for (int ky = 0; ky < KH; ++ky) {
+                for (int q = 0; q < P; ++q) A[r][q] = 0;
+#pragma unroll
+                for (int i = 0; i < NC; ++i) colsum[r][i] = 0;
+            }
+#pragma unroll
+            for (int ir = 0; ir < NR; ++ir) {
 #pragma unroll
                 for (int i = 0; i < NC; ++i) {
-                    const uint32_t code = cbuf[(ky * NC + i) * 32];
-                    const uint8_t *base = tab_lane + (code >> 1) * 128u + ky * KW * kDwTapBytes;
+                    const uint32_t code = cbuf[(ir * NC + i) * 32];
+                    const uint8_t *base = tab_lane + (code >> 1) * 128u;
                     const uint32_t sel = 0x4410u + (code & 1u) * 0x22u;
                     const int32_t cv = p.sgn ? (int32_t)(int8_t)code : (int32_t)code;
 #pragma unroll
-                    for (int kx = 0; kx < KW; ++kx) {
-                        const int q = (i - kx) / SW;  // output pixel reading column i at tap kx
-                        if (i - kx >= 0 && (i - kx) % SW == 0 && q < P) {
-                            const uint32_t w = *reinterpret_cast<const uint32_t *>(base + kx * kDwTapBytes);
-                            A[q] += __byte_perm(w, 0, sel);  // the entry of this code (axconv.py:136-146)
-                            sp[q] += cv;
+                    for (int r = 0; r < R; ++r) {
+                        const int ky = ir - r;  // kernel row of input row ir for output row r (stride 1 if R > 1)
+                        if (ky < 0 || ky >= KH) continue;
+                        colsum[r][i] += cv;
+#pragma unroll
+                        for (int kx = 0; kx < KW; ++kx) {
+                            const int q = (i - kx) / SW;  // output pixel reading column i at tap kx
+                            if (i - kx >= 0 && (i - kx) % SW == 0 && q < P) {
+                                const uint32_t w = *reinterpret_cast<const uint32_t *>(
+                                    base + (ky * KW + kx) * kDwTapBytes);
+                                A[r][q] += __byte_perm(w, 0, sel);  // the entry of this code (axconv.py:136-146)
+                            }
                         }
                     }
                 }
             }
-            __syncwarp();  // every lane read the buffer before the fetch two strips on overwrites it
+            __syncwarp();  // every lane read the buffer before the fetch two units on overwrites it
             buf ^= 1;
 #pragma unroll
-            for (int q = 0; q < P; ++q) {
-                if (ch < p.c && ox0 + q < (int)p.ow) {
-                    const int32_t Ai = (int32_t)A[q];  // exact: |A - ubias| <= 9 * 32768
-                    const int64_t o = (((int64_t)b * p.oh + oy) * p.ow + ox0 + q) * p.c + ch;
-                    if (p.acc_out) p.acc_out[o] = Ai - ubias;
-                    // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254), exact in int32 here
-                    const int32_t corr = Ai - zp2 * sp[q] + cc;
-                    float y = __fadd_rn(__double2float_rn(scale * (double)corr), bias);  // :256; graph.py:268-269
-                    if (has_res) y = __fadd_rn(y, __ldg(p.residual + o));               // graph.py:282-286
-                    if (relu) y = (y > 0.0f || y != y) ? y : 0.0f;                      // graph.py:276-277
-                    p.out[o] = y;
-                    track(y, tmin, tmax, nonfinite);
+            for (int r = 0; r < R; ++r) {
+                const int oy = (int)oy0 + r;
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                    if (ch < p.c && ox0 + q < (int)p.ow && oy < (int)p.oh) {
+                        const int32_t Ai = (int32_t)A[r][q];  // exact: |A - ubias| <= 9 * 32768
+                        const int32_t sp = colsum[r][q * SW] + colsum[r][q * SW + 1] + colsum[r][q * SW + 2];
+                        const int64_t o = (((int64_t)b * p.oh + oy) * p.ow + ox0 + q) * p.c + ch;
+                        if (p.acc_out) p.acc_out[o] = Ai - ubias;
+                        // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254), exact in int32 here
+                        const int32_t corr = Ai - zp2 * sp + cc;
+                        float y = __fadd_rn(__double2float_rn(scale * (double)corr), bias);  // :256; graph.py:268-269
+                        if (has_res) y = __fadd_rn(y, __ldg(p.residual + o));               // graph.py:282-286
+                        if (relu) y = (y > 0.0f || y != y) ? y : 0.0f;                      // graph.py:276-277
+                        p.out[o] = y;
+                        track(y, tmin, tmax, nonfinite);
+                    }
                 }
             }
         }
@@ -426,22 +451,24 @@ extern "C" int axb_depthwise_lut(const axb_conv_desc *d, const axb_lut *lut, voi
     k.sgn = lut->is_signed;
     k.taps = d->kh * d->kw;
     if (d->ftable && d->variant != 1 && k.taps == 9 && d->kh == 3 && d->dh == 1 && d->dw == 1 &&
-        (d->sw == 1 || d->sw == 2) &&
+        ((d->sw == 1 && d->sh == 1) || d->sw == 2) &&
         d->n * d->oh * d->ow < ((int64_t)1 << 31) && dw_rs_enabled()) {
-        // row-strip kernel: strips of 16 (stride 1) / 8 (stride 2) output pixels per warp
-        constexpr int NW = 16, P = 16;
+        // row-strip kernel: 2 rows x 8 pixels per warp unit at stride 1, 1 row x 8 pixels at stride 2
+        constexpr int NW = 16, P = 8;
         k.dwtable = reinterpret_cast<const uint32_t *>(d->ftable);
         k.fd_oh = make_fastdiv((uint32_t)d->oh);
-        const int ps = d->sw == 1 ? P : P / 2;  // output pixels per strip
-        const int32_t nstrips = (int32_t)((d->ow + ps - 1) / ps);
-        const int64_t units = ((d->c + 31) / 32) * d->n * d->oh * nstrips;
-        if (d->n * d->oh * nstrips >= ((int64_t)1 << 31)) return set_error(AXB_E_VALUE, "depthwise conv too large");
-        const size_t smem = d->sw == 1 ? dw_rs_smem<1, P, NW>() : dw_rs_smem<2, P / 2, NW>();
-        auto fn = d->sw == 1 ? depthwise_rs_kernel<1, P, NW> : depthwise_rs_kernel<2, P / 2, NW>;
+        const bool s1 = d->sw == 1 && d->sh == 1;
+        const int rows = s1 ? 2 : 1;
+        const int32_t nstrips = (int32_t)((d->ow + P - 1) / P);
+        const int32_t ohr = (int32_t)((d->oh + rows - 1) / rows);
+        const int64_t units = ((d->c + 31) / 32) * d->n * ohr * nstrips;
+        if (d->n * ohr * nstrips >= ((int64_t)1 << 31)) return set_error(AXB_E_VALUE, "depthwise conv too large");
+        const size_t smem = s1 ? dw_rs_smem<1, P, 2, NW>() : dw_rs_smem<2, P, 1, NW>();
+        auto fn = s1 ? depthwise_rs_kernel<1, P, 2, NW> : depthwise_rs_kernel<2, P, 1, NW>;
         static int configured[2] = {-1, -1};
         int dev = 0;
         cudaGetDevice(&dev);
-        const int which = d->sw == 1;
+        const int which = s1;
         if (configured[which] != dev) {
             if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return set_error(AXB_E_CUDA, "cannot raise dynamic shared memory for depthwise_rs_kernel");
@@ -450,7 +477,8 @@ extern "C" int axb_depthwise_lut(const axb_conv_desc *d, const axb_lut *lut, voi
         int64_t grid = sm_count();
         if (grid > (units + NW - 1) / NW) grid = (units + NW - 1) / NW;
         if (grid < 1) grid = 1;
-        fn<<<(int)grid, NW * 32, smem, (cudaStream_t)stream>>>(k, make_fastdiv((uint32_t)nstrips), nstrips);
+        fn<<<(int)grid, NW * 32, smem, (cudaStream_t)stream>>>(k, make_fastdiv((uint32_t)nstrips), nstrips,
+                                                               make_fastdiv((uint32_t)ohr), ohr);
         set_last_kernel("depthwise_rs");
         return check_launch("depthwise_rs");
     }
