@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, F
     const uint32_t U = (uint32_t)(p.n * ohr) * (uint32_t)nstrips;  // units per channel block (< 2^31)
     const int64_t total = (int64_t)nb * U;
     const int64_t lo = total * blockIdx.x / gridDim.x, hi = total * (blockIdx.x + 1) / gridDim.x;
-    const bool has_res = p.residual != nullptr, relu = p.relu != 0;
+    const bool has_res = p.residual != nullptr, relu = p.relu != 0, has_acc = p.acc_out != nullptr;
     float tmin = INFINITY, tmax = -INFINITY;
     int nonfinite = 0;
     uint32_t phase = 0;
@@ -375,16 +375,18 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, F
             }
             __syncwarp();  // every lane read the buffer before the fetch two units on overwrites it
             buf ^= 1;
+            const int nq = min(P, (int)p.ow - ox0);  // pixels of the strip inside the row
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int oy = (int)oy0 + r;
+                if (ch >= p.c || oy >= (int)p.oh) continue;
+                const int64_t o0 = (((int64_t)b * p.oh + oy) * p.ow + ox0) * p.c + ch;  // output (oy, ox0, ch)
 #pragma unroll
                 for (int q = 0; q < P; ++q) {
-                    if (ch < p.c && ox0 + q < (int)p.ow && oy < (int)p.oh) {
+                    if (q < nq) {
                         const int32_t Ai = (int32_t)A[r][q];  // exact: |A - ubias| <= 9 * 32768
                         const int32_t sp = colsum[r][q * SW] + colsum[r][q * SW + 1] + colsum[r][q * SW + 2];
-                        const int64_t o = (((int64_t)b * p.oh + oy) * p.ow + ox0 + q) * p.c + ch;
-                        if (p.acc_out) p.acc_out[o] = Ai - ubias;
+                        const int64_t o = o0 + (int64_t)q * p.c;
                         // corr = A - zp2*S_p - zp1*S_f + K*zp1*zp2 (axconv.py:249-254), exact in int32 here
                         const int32_t corr = Ai - zp2 * sp + cc;
                         float y = __fadd_rn(__double2float_rn(scale * (double)corr), bias);  // :256; graph.py:268-269
@@ -392,6 +394,7 @@ __global__ void __launch_bounds__(NW * 32, 1) depthwise_rs_kernel(const DwK p, F
                         if (relu) y = (y > 0.0f || y != y) ? y : 0.0f;                      // graph.py:276-277
                         p.out[o] = y;
                         track(y, tmin, tmax, nonfinite);
+                        if (has_acc) p.acc_out[o] = Ai - ubias;
                     }
                 }
             }
