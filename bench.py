@@ -158,7 +158,7 @@ def _free_port() -> int:
 
 def launch_ranks(args, argv) -> int:
     """Re-run this script under torch.distributed.run with ``args.gpus`` local ranks."""
-    if not args.stub:
+    if not args.stub and not args.share_device:
         import torch
 
         have = torch.cuda.device_count()
@@ -659,6 +659,9 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--stub", action="store_true", help="CPU/gloo synthetic step: launcher + sharding + JSON only")
+    ap.add_argument("--share-device", action="store_true",
+                    help="test mode: every rank on cuda:0 with gloo collectives (the multi-rank device path on a "
+                         "one-GPU box; its timings are not a scaling measurement)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-numba", action="store_true", help="skip the real-reference (numba) CPU timing")
@@ -680,7 +683,7 @@ def main(argv=None):
             sys.exit(launch_ranks(args, argv))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.share_device else int(os.environ.get("LOCAL_RANK", "0"))
     spec = workload_spec(args.workload, args.lut)
     batch = args.batch or spec["batch"]
     from paper_2002_09481_b200 import resnet
@@ -702,7 +705,7 @@ def main(argv=None):
     if world > 1:
         import torch.distributed as dist
 
-        if args.stub:
+        if args.stub or args.share_device:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
@@ -727,6 +730,8 @@ def main(argv=None):
     agree = (pred == labels[None, :]).sum(1) if len(pred) else np.zeros(0, np.int64)
     cnt = torch.tensor([int(agree.sum()), batch * len(units)], dtype=torch.int64, device=dev)
     t = torch.tensor([res["total_ms"], res["e2e_ms"], res["conv_ms"]], dtype=torch.float64, device=dev)
+    if args.share_device:  # gloo collectives: host tensors
+        logits, cnt, t = logits.cpu(), cnt.cpu(), t.cpu()
     gathered, cnt, t = exchange_results(logits, cnt, t)
     unit_lists = [units]
     if dist is not None:
@@ -780,6 +785,8 @@ def main(argv=None):
     max_mhz = float(peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0)
     y0 = res["logits"][0].cpu().numpy() if len(units) else None
     line["parity"] = parity_block(args, spec, batch, y0) if y0 is not None else {"status": "unchecked"}
+    if args.share_device:
+        line["shared_device"] = True  # test mode: all ranks on cuda:0 (not a scaling measurement)
     # rank 0's device time alone feeds the per-kernel blocks (same GPU model on every rank)
     line["roofline"] = roofline_block(args, res, sm_count, max_mhz, clocks.get("sm_mhz"), res["total_ms"])
     hbm_peak = float(peaks.get("hbm_gbs") or 6550.0)

@@ -57,3 +57,18 @@ def test_range_batches_two_ranks():
 def test_single_process_stub_unchanged():
     lines = _bench("--stub", "--workload", "r8", "--steps", "2", "--batch", "16")
     assert len(lines) == 1 and lines[0]["n_gpus"] == 1 and lines[0]["units"]["per_rank"] == [1]
+
+
+@pytest.mark.gpu
+def test_two_ranks_share_one_gpu_device_path():
+    """The multi-rank DEVICE path end to end on a one-GPU box: the launcher, two ranks each running its own
+    range-batch through the CUDA-graph executor, the exchange (gloo here: NCCL needs one GPU per rank),
+    the max-over-ranks timing, rank 0's logits bit-exact against the reference's."""
+    lines = _bench("--gpus", "2", "--share-device", "--workload", "r8", "--steps", "2", "--warmup", "3",
+                   "--no-cpu-baseline", "--no-autotune", timeout=900)
+    assert len(lines) == 1, lines
+    ln = lines[0]
+    assert ln["n_gpus"] == 2 and ln["shared_device"] is True and ln["scaling"] == "weak"
+    assert ln["units"] == {"kind": "range-batches", "per_rank": [1, 1], "total": 2, "covered_once": True}
+    assert ln["parity"]["status"] == "bit-exact", ln["parity"]
+    assert ln["value"] > 0 and ln["e2e"]["value"] > 0
