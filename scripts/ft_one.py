@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--node", required=True)
     ap.add_argument("--variant", required=True)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--residual", action="store_true", help="fuse a residual add (an fp32 tensor of the output's shape)")
     args = ap.parse_args()
     spec = workload_spec(args.workload, "trunc2")
     imgs, _ = make_images(spec["kind"], args.batch or spec["batch"], seed=1000)
@@ -40,9 +41,14 @@ def main():
     layer = ConvLayer(a["filters"], (a["f_min"], a["f_max"]), a["lut"], _geometry(a), a.get("bias"))
     layer.set_input_params(float(x.min()), float(x.max()))
     flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    res = None
+    if args.residual:
+        y0 = layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(),
+                       ft_variant=names[args.variant])
+        res = torch.randn_like(y0)
     for _ in range(args.reps):
         prof = []
-        layer.run(x, None, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(), profile=prof,
+        layer.run(x, None, residual=res, out_flag=flags[0].data_ptr(), quant_flag=flags[1].data_ptr(), profile=prof,
                   ft_variant=names[args.variant])
         torch.cuda.synchronize()
         print(args.variant, round(prof[0][0].elapsed_time(prof[0][1]), 4), "ms")
