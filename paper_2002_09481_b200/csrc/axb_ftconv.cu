@@ -621,24 +621,26 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ftcm(const ConvK p) {
                  AXB_FLAG_OUT_NONFINITE);
 }
 
-// ---------------------------------------------------------------- 64-channel code-major variant (C64)
-// Same products, laid out C64[cb][k][a][32 pairs]: the 64 channels of block cb at row k and activation
-// code a are 128 contiguous bytes = all 32 banks.  Lanes = (pixel slot ps = lane>>3, octant o = lane&7):
-// one LDS.128 at a*128 + o*16 returns 4 pairs (8 products) of one pixel, and the 8 lanes of a quarter-warp
-// -- the unit the shared memory serves a 128-bit request in -- are ONE pixel reading one whole 128-byte
-// row: every quarter is one wavefront whatever the codes are.  A warp instruction = 4 pixels x 64 channels
-// = 256 products in exactly 4 wavefronts, the shared-memory peak (64 products per wavefront), with no
-// data-dependent bank conflicts (the pair-major and 32-channel layouts lose 30-50% of their wavefronts to
-// conflicts on real activations).  Table bytes staged per product = 512 / BM (BM = WARPS * 4 * J pixels).
+// ---------------------------------------------------------------- CX family (lutconv_cx): c64 / c32 / c16
+// Same products, laid out CX[blk][k][a][32 words]: at 64-channel blocks (C64) the 64 channels of block
+// blk at row k and activation code a are 128 contiguous bytes = all 32 banks.  Lanes = (pixel slot
+// ps = lane / 8, octant o = lane % 8): one LDS.128 at a*128 + o*16 returns 4 pairs (8 products) of one
+// pixel, and the 8 lanes of a quarter-warp -- the unit the shared memory serves a 128-bit request in --
+// are ONE pixel reading one whole 128-byte row: every quarter is one wavefront whatever the codes are.
+// A warp instruction = 4 pixels x 64 channels = 256 products in exactly 4 wavefronts, the shared-memory
+// peak (64 products per wavefront), with no data-dependent bank conflicts (the pair-major and 32-channel
+// layouts lose 30-50% of their wavefronts to conflicts on real activations).  Narrower blocks (32 / 16
+// channels) repeat the block's words across the 128-byte row (below).
 // Registers: a lane holds 8 accumulator words per pixel (J pixels), so the activation codes do not live
-// in registers ahead of use: each warp stages its PXW = 4*J pixels' next 16-row chunk in its own shared
-// buffer with cp.async (lane L copies pixels L, L+32, ...: 16 bytes each), lanes read CR rows per pixel
-// (LDS.64 for CR = 8, LDS.32 for CR = 4 -- half the code registers), and lane L sums its staged pixels'
-// codes (S_p, DP4A) -- shuffled to the pixel's lanes at the end.
-// Why J = 16: the table stages are the kernel's L2 traffic, 512 / BM bytes per product (32 KiB per row
-// and 64-channel block, read once per BM-pixel tile).  With BM = 384 (J = 8, 12 warps) that is 1.33 B per
-// product -- at ~8.8e12 products/s, 11 TB/s of L2->SM traffic, the chip's L2 read ceiling -- so the tile
-// has to grow: J = 16 at 8 or 10 warps (BM = 512 / 640) cuts it to 1.0 / 0.8 B per product.
+// in registers ahead of use: each warp stages its PXW pixels' next 16-row chunk in its own shared buffer
+// with cp.async (lane L copies pixels L, L+32, ...: 16 bytes each), lanes read CR rows per pixel (LDS.64
+// for CR = 8, LDS.32 for CR = 4 -- half the code registers, what lets J = 16..20 fit), and lane L sums
+// its staged pixels' codes (S_p, DP4A) -- shuffled to the pixel's lanes in the epilogue.
+// Table staging: 512 / BM bytes per product at 64-channel blocks (32 KiB per row and block, read once per
+// BM-pixel tile), moved by TMA into a 3-slot ring of 2-row stages; BM is as large as the register file
+// allows (J = 16 / 20 at 8 consumer warps: 1.0 / 0.8 B per product).  A producer warpgroup (PW = 1)
+// refills a slot as soon as the last consumer released it; the last partial wave of tiles is cut into K
+// pieces (tail split, launch_cx); kpad <= kCxMaxK keeps the epilogue's correction exact in 32 bits.
 constexpr int kCxMaxK = 8192;  // CX kernels: the 32-bit epilogue correction is exact up to this K
 constexpr int kC64Pairs = 32;                   // channel pairs per 64-channel block
 constexpr int kC64RowWords = 256 * kC64Pairs;   // one (block, row) slice: 256 codes x 32 pairs
