@@ -304,7 +304,7 @@ def make_bench() -> dict:
 
     lut = T.truncated_lut(T.Signedness.SIGNED, 2)
     out = {}
-    which = [a for a in sys.argv[1:] if a in ("r8", "r50", "mbv1")] or ["r8", "r50", "mbv1"]
+    which = [a for a in sys.argv[1:] if a in ("r8", "r50", "mbv1", "r62sweep")] or ["r8", "r50", "mbv1", "r62sweep"]
     path = HERE / "bench.npz"
     if path.exists():
         out.update(dict(np.load(path)))
@@ -317,6 +317,22 @@ def make_bench() -> dict:
     if "mbv1" in which:
         x, _ = datasets.synthetic_imagenet(256, seed=BENCH_SEED)
         run_reference("mbv1", resnet.mobilenet_v1(lut, seed=0), x, out)
+    if "r62sweep" in which:
+        # config 4: the sweep's first candidate network (bench.py sweep_luts()[0], truncated_lut(signed, 0))
+        # on the sweep batch synthetic_cifar10(1000, 1000); logits only (63 traced convs at 1000 images
+        # would be 4 GB)
+        sys.path.insert(0, str(HERE.parent.parent))
+        import bench
+
+        x, _ = datasets.synthetic_cifar10(1000, seed=BENCH_SEED)
+        nodes = resnet.cifar_resnet(10, bench.sweep_luts()[0], seed=0)
+        for n in nodes:
+            if "filters" in n["attrs"]:
+                n["attrs"]["filters"] = np.ascontiguousarray(n["attrs"]["filters"], np.float32)
+        y = axemu.run(to_reference_graph(nodes), Tensor4(x, Layout.NHWC), "gemm").data
+        out["r62sweep_logits_sha"] = np.frombuffer(bytes.fromhex(sha(y)), np.uint8)
+        out["r62sweep_argmax"] = y.reshape(1000, -1).argmax(1)
+        print("r62sweep argmax distinct", len(set(out["r62sweep_argmax"].tolist())), flush=True)
     return out
 
 

@@ -4,6 +4,7 @@ Bit-exact for fp32 outputs (bit patterns), raw int64 accumulators and argmax.
 """
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -385,6 +386,27 @@ def test_benchmarked_configs_bit_exact_vs_reference(arch):
     gg.capture(tuple(xd.shape))
     y2 = gg.replay(xd)
     assert _sha(y2) == g[f"{arch}_logits_sha"].tobytes()
+
+
+def test_sweep_first_candidate_full_batch_vs_reference():
+    """Config 4 at bench.py's sweep batch: ResNet-62 with the first candidate table (truncated_lut(signed,
+    0)) on synthetic_cifar10(1000, 1000) -- all 1000 logits rows bit-identical to the real reference's
+    graph.run (tests/golden/bench.npz r62sweep_logits_sha).  (This deep random network's argmax is one
+    class for every image; the check is the logits' bits.)"""
+    import sys
+
+    torch = _torch()
+    from paper_2002_09481_b200 import datasets, resnet
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+
+    g = load_golden("bench")
+    x = datasets.synthetic_cifar10(1000, seed=1000)[0]
+    y = GpuGraph(resnet.cifar_resnet(10, bench.sweep_luts()[0], seed=0)).run(torch.from_numpy(x).cuda())
+    assert _sha(y) == g["r62sweep_logits_sha"].tobytes()
+    assert np.array_equal(y.reshape(1000, -1).argmax(1).cpu().numpy(), g["r62sweep_argmax"])
 
 
 def test_r50_full_batch_grid_invariant():
