@@ -23,4 +23,5 @@ for n in s0b1.b s1b1.c r8s0b0b; do
 done
 python scripts/step_breakdown.py $G/launches_r50_$T.csv $P/r2_${T}_ncu_s0b1.b.md 108 > /dev/null
 python scripts/traffic.py $G/traffic_r50_$T.csv r50
+[ -f $G/traffic_r8_$T.csv ] && python scripts/traffic.py $G/traffic_r8_$T.csv r8
 echo "collected $T"

@@ -41,4 +41,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:lutconv -c 54 \
     --csv --log-file gpurun_out/traffic_r50_$T.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     --tuned-from $TUNED > /dev/null 2>&1
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:lutconv -c 10 \
+    --csv --log-file gpurun_out/traffic_r8_$T.csv python bench.py --workload r8 --steps 1 --warmup 3 --no-cpu-baseline \
+    --tuned-from gpurun_out/tuned_r8_$T.json > /dev/null 2>&1
 du -sh gpurun_out
