@@ -1295,12 +1295,18 @@ static int launch_cx(int op, const ConvK &k, int sm_limit, cudaStream_t s, const
     kk.split_L = split_L;
     kk.split_s = split_s;
     void *ws = nullptr;
+    const size_t ws_bytes = (size_t)split_L * split_s * (WARPS * 32) * c64_split_words(J, CB) * 4;
+    const size_t cnt_bytes = (size_t)split_L * 4;
     if (split_s > 1) {
         keep_pool_memory(dev);
-        const size_t ws_bytes = (size_t)split_L * split_s * (WARPS * 32) * c64_split_words(J, CB) * 4;
-        const size_t cnt_bytes = (size_t)split_L * 4;
-        if (cudaMallocAsync(&ws, ws_bytes + cnt_bytes, s) != cudaSuccess)
-            return set_error(AXB_E_CUDA, "cannot allocate the c64 tail-split workspace");
+        if (cudaMallocAsync(&ws, ws_bytes + cnt_bytes, s) != cudaSuccess) {
+            cudaGetLastError();  // no workspace: run without the split (same results, a ragged last wave)
+            ws = nullptr;
+            kk.split_L = 0;
+            kk.split_s = 1;
+        }
+    }
+    if (ws) {
         kk.split_ws = static_cast<uint32_t *>(ws);
         kk.split_cnt = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(ws) + ws_bytes);
         if (cudaMemsetAsync(kk.split_cnt, 0, cnt_bytes, s) != cudaSuccess) {
