@@ -593,7 +593,9 @@ def roofline_block(args, res, sm_count, max_mhz, sampled, total_ms):
         "conflict_basis": "profiles/conflicts.json (ncu l1tex shared-load bank conflicts / wavefronts)",
         "lds16_lookup_roofline": round(lds16 / 1e9, 2),
         "frac_vs_lds16_lookup_roofline": round(achieved / lds16, 4),
-        "traffic": traffic, "traffic_unit": "DRAM bytes per LUT-conv launch: ncu dram__bytes_read.sum + dram__bytes_write.sum averaged over one step's conv launches (cold cache, tuned kernels; profiles/traffic_<workload>.json)",
+        "traffic": traffic,
+        "traffic_unit": ("DRAM bytes per LUT-conv launch: ncu dram__bytes_read.sum + dram__bytes_write.sum averaged "
+                         "over one step's conv launches (cold cache, tuned kernels; profiles/traffic_<workload>.json)"),
         "algorithmic_bytes_per_launch": int(conv_algo_bytes / max(launches, 1)),
         "conv_launches_per_step": launches,
         "conv_share_of_step": round(conv_ms / step_ms, 4) if total_ms else None,
