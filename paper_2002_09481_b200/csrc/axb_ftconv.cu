@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lutconv_ft(const ConvK p) {
                     }
                     produce();
                 }
-                mbar_wait(full + slot, (uint32_t)((g / ST) & 1));
+                mbar_wait_sleep(full + slot, (uint32_t)((g / ST) & 1));
                 const uint32_t *stab = tab + slot * (STAGE_BYTES / 4);
 #pragma unroll
                 for (int kl = 0; kl < KS; ++kl) {
