@@ -666,6 +666,9 @@ def main(argv=None):
     ap.add_argument("--share-device", action="store_true",
                     help="test mode: every rank on cuda:0 with gloo collectives (the multi-rank device path on a "
                          "one-GPU box; its timings are not a scaling measurement)")
+    ap.add_argument("--launch", action="store_true",
+                    help="re-launch under torch.distributed.run even for --gpus 1: the process group (NCCL) and "
+                         "the logits/counts exchange then run with a single rank (evidence on a one-GPU box)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-numba", action="store_true", help="skip the real-reference (numba) CPU timing")
@@ -680,7 +683,7 @@ def main(argv=None):
     if args.warmup < 3:
         args.warmup = 3
 
-    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or args.launch):
         if args.impl == "reference":  # the CPU arm runs once, on "rank 0"
             os.environ.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
         else:
@@ -706,7 +709,7 @@ def main(argv=None):
     else:
         torch.cuda.set_device(local)
         dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # launched ranks (also a one-rank --launch)
         import torch.distributed as dist
 
         if args.stub or args.share_device:
@@ -770,6 +773,10 @@ def main(argv=None):
         "units": units_info,
         "agreement_with_labels": round(float(cnt[0]) / float(cnt[1]), 4) if float(cnt[1]) else None,
     }
+    if dist is not None:  # the one exchange after the timed work (dist.exchange_results)
+        line["exchange"] = {"backend": dist.get_backend(), "ranks": world,
+                            "ops": "all_gather(unit counts, logits) + all_reduce(counts SUM, times MAX)",
+                            "logits_rows_gathered": sum(int(g.shape[0]) for g in gathered)}
     if args.stub:
         line["stub"] = "synthetic host step (no GPU): launcher, sharding, gather and JSON path only"
         line["logits_gathered"] = list(gathered.shape) if hasattr(gathered, "shape") else [len(gathered)]

@@ -24,4 +24,7 @@ done
 python scripts/step_breakdown.py $G/launches_r50_$T.csv $P/r2_${T}_ncu_s0b1.b.md 108 > /dev/null
 python scripts/traffic.py $G/traffic_r50_$T.csv r50
 [ -f $G/traffic_r8_$T.csv ] && python scripts/traffic.py $G/traffic_r8_$T.csv r8
+[ -f $G/bench_r50_nccl_$T.json ] && cp $G/bench_r50_nccl_$T.json $P/r2_${T}_bench_r50_nccl.json
+[ -f $G/nccl_init_$T.log ] && grep -E "NCCL INFO|launching" $G/nccl_init_$T.log | head -60 > $P/r2_${T}_nccl_init.txt
+[ -f $G/ft_stress_$T.txt ] && cp $G/ft_stress_$T.txt $P/r2_${T}_ft_stress.txt
 echo "collected $T"

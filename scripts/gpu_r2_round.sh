@@ -45,3 +45,10 @@ timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
     --csv --log-file gpurun_out/traffic_r8_$T.csv python bench.py --workload r8 --steps 1 --warmup 3 --no-cpu-baseline \
     --tuned-from gpurun_out/tuned_r8_$T.json > /dev/null 2>&1
 du -sh gpurun_out
+# one-rank torchrun launch: NCCL communicator + the logits/counts exchange on the device (INIT log kept)
+timeout 900 python bench.py --gpus 1 --launch --steps 5 --no-cpu-baseline --tuned-from $TUNED \
+    > gpurun_out/bench_r50_nccl_$T.log 2> gpurun_out/nccl_init_$T.log
+tail -1 gpurun_out/bench_r50_nccl_$T.log > gpurun_out/bench_r50_nccl_$T.json
+# nondeterminism stress of every ftable-kernel variant (compute-sanitizer is closed on this pool)
+timeout 900 python scripts/ft_stress.py 10 > gpurun_out/ft_stress_$T.txt 2>&1
+tail -3 gpurun_out/ft_stress_$T.txt

@@ -59,6 +59,27 @@ def test_single_process_stub_unchanged():
     assert len(lines) == 1 and lines[0]["n_gpus"] == 1 and lines[0]["units"]["per_rank"] == [1]
 
 
+def test_one_rank_launch_runs_the_exchange():
+    """--launch: even --gpus 1 goes through torch.distributed.run, the process group and the exchange."""
+    lines = _bench("--gpus", "1", "--launch", "--stub", "--workload", "r8", "--steps", "2", "--batch", "16")
+    assert len(lines) == 1
+    ln = lines[0]
+    assert ln["n_gpus"] == 1 and ln["units"]["per_rank"] == [1]
+    assert ln["exchange"]["backend"] == "gloo" and ln["exchange"]["ranks"] == 1
+    assert ln["exchange"]["logits_rows_gathered"] == 1
+
+
+@pytest.mark.gpu
+def test_one_rank_nccl_exchange_on_device():
+    """The NCCL communicator and the logits/counts exchange on the B200 (one rank: the box has one GPU)."""
+    lines = _bench("--gpus", "1", "--launch", "--workload", "r8", "--steps", "2", "--warmup", "3",
+                   "--no-cpu-baseline", "--no-autotune", timeout=900)
+    assert len(lines) == 1, lines
+    ln = lines[0]
+    assert ln["exchange"]["backend"] == "nccl" and ln["exchange"]["ranks"] == 1
+    assert ln["parity"]["status"] == "bit-exact", ln["parity"]
+
+
 @pytest.mark.gpu
 def test_two_ranks_share_one_gpu_device_path():
     """The multi-rank DEVICE path end to end on a one-GPU box: the launcher, two ranks each running its own
