@@ -167,8 +167,10 @@ def launch_ranks(args, argv) -> int:
                                                          "devices"}), flush=True)
             return 1
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    # every rank prints its communicator line (ncclCommInitRankConfig ... nranks N); a box-level NCCL_DEBUG
+    # (seen: one that printed only the version line) would hide it
+    env["NCCL_DEBUG"] = "INFO"
+    env["NCCL_DEBUG_SUBSYS"] = "INIT"
     env.setdefault("OMP_NUM_THREADS", "4")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()), *argv]

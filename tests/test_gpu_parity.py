@@ -1038,3 +1038,54 @@ def test_graph_frees_intermediates_after_last_reader():
     torch.cuda.synchronize()
     freed = torch.cuda.max_memory_allocated() - base
     assert freed < 0.35 * keep_all, (freed, keep_all)
+
+
+def _ord2f(i: int) -> float:
+    b = i if i >= 0 else i ^ 0x7FFFFFFF
+    return float(np.array([b], np.int32).view(np.float32)[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bad", [None, np.nan, np.inf, -np.inf])
+@pytest.mark.parametrize("relu", [False, True])
+def test_cx_output_range_and_nonfinite_flag(bad, relu):
+    """The CX epilogue's fused next-layer range (graph.py:270-275 over the conv output) is the exact
+    min/max of what it stored, and a non-finite output (here from the residual Add, graph.py:282-286)
+    raises AXB_FLAG_OUT_NONFINITE -- for every CX variant, ragged tiles and the tail split included."""
+    torch = _torch()
+    from paper_2002_09481_b200 import _lib
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.layer import ConvLayer
+
+    lib = _lib.load()
+    rng = np.random.default_rng(11)
+    x = torch.relu(torch.from_numpy(rng.standard_normal((2, 9, 11, 32)).astype(np.float32))).cuda()
+    f = (rng.standard_normal((3, 3, 32, 64)) * 0.05).astype(np.float32)
+    lay = ConvLayer(f, (float(f.min()), float(f.max())), T.truncated_lut(T.Signedness.SIGNED, 2),
+                    T.ConvGeometry(padding="same"),
+                    bias=(rng.standard_normal(64) * 0.05).astype(np.float32))
+    lay.set_input_params(0.0, float(x.max()))
+    res = torch.from_numpy(rng.standard_normal((2, 9, 11, 64)).astype(np.float32))
+    if bad is not None:
+        res[1, 3, 4, 5] = float(bad)
+    res = res.cuda()
+    n = 0
+    for v in range(1, lib.axb_ft_variant_count()):
+        if not lib.axb_ft_variant_name(v).decode().startswith("c") or \
+                64 % LAYOUT_BLOCK[lib.axb_ft_variant_layout(v)]:
+            continue
+        orng = torch.tensor([2**31 - 1, -2**31], dtype=torch.int32, device="cuda")
+        flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+        y = lay.run(x, None, residual=res, relu=relu, out_range=orng.data_ptr(), out_flag=flags[0].data_ptr(),
+                    quant_flag=flags[1].data_ptr(), ft_variant=v)
+        torch.cuda.synchronize()
+        name = lib.axb_ft_variant_name(v).decode()
+        fl = int(flags[0].item())
+        if bad is None or (relu and bad == -np.inf):  # ReLU after the Add: -inf -> 0, the output is finite
+            assert fl & _lib.FLAG_OUT_NONFINITE == 0, name
+            lo, hi = (_ord2f(int(t)) for t in orng.tolist())
+            assert lo == float(y.min()) and hi == float(y.max()), name
+        else:
+            assert fl & _lib.FLAG_OUT_NONFINITE, name
+        n += 1
+    assert n >= 5
