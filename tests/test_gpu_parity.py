@@ -1089,3 +1089,67 @@ def test_cx_output_range_and_nonfinite_flag(bad, relu):
             assert fl & _lib.FLAG_OUT_NONFINITE, name
         n += 1
     assert n >= 5
+
+
+@pytest.mark.gpu
+def test_quantizer_flat_path_sweep():
+    """The flat quantizer (unpadded input, no per-pixel sums: what every 1x1 CX layer runs) vs
+    quantize_values (quantizer.py:120-131) on dense near-tie sweeps, all modes, ragged unit tails
+    (element counts not a multiple of the 512-float warp unit), host and device coefficients, and the
+    non-finite flag (tensor.py:143-149 -> ValueError)."""
+    torch = _torch()
+    from paper_2002_09481_b200 import _lib
+
+    lib = _lib.load()
+    s = torch.cuda.current_stream().cuda_stream
+    rng = np.random.default_rng(78)
+    rounds = {O.HALF_AWAY: 0, O.HALF_EVEN: 1, O.TOWARD_ZERO: 2}
+    for trial in range(12):
+        mode = (O.SIGNED, O.UNSIGNED)[trial % 2]
+        rname = list(rounds)[trial % 3]
+        mn = float(-abs(rng.standard_normal()) * 10 ** rng.uniform(-3, 3)) if trial % 4 else 0.0
+        mx = float(abs(rng.standard_normal()) * 10 ** rng.uniform(-3, 3))
+        mn, mx = float(np.float32(mn)), float(np.float32(mx))  # a device range holds float32 extremes
+        scale, zp = O.compute_coeffs(mn, mx, mode, rname)
+        lo, _ = O.bounds(mode)
+        k = np.arange(-300, 300, dtype=np.float64)
+        base = np.concatenate([(k + 0.5 - zp + lo) * scale, (k - zp + lo) * scale]).astype(np.float32)
+        near = (base.view(np.int32)[:, None] + np.arange(-3, 4, dtype=np.int32)[None, :]).reshape(-1).view(np.float32)
+        vals = np.concatenate([near, rng.uniform(mn * 1.5, mx * 1.5, 70000).astype(np.float32), [mn, mx]])
+        vals = vals[np.isfinite(vals)].astype(np.float32)
+        hp_ = _lib.QParams()
+        _lib.check(lib.axb_coeffs_host(mn, mx, int(mode == O.SIGNED), rounds[rname], hp_))
+        prm = torch.zeros(_lib.QPARAMS_BYTES, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.axb_params_upload(hp_, prm.data_ptr(), s))
+        ordr = torch.from_numpy(np.array([mn, mx], np.float32).view(np.int32)).cuda()
+        ordr = torch.where(ordr >= 0, ordr, ordr ^ 0x7FFFFFFF).to(torch.int32)
+        for c in (16, 64, 256):
+            v = vals[: len(vals) // c * c]
+            want = O.quantize_values(v, scale, zp, mode, rname)
+            n = len(v) // c
+            x = torch.from_numpy(v.reshape(1, 1, n, c)).cuda()
+            for dev_range in (False, True):
+                codes = torch.full((n * c,), 0xAB, dtype=torch.uint8, device="cuda")
+                fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+                if dev_range:
+                    p2 = torch.zeros(_lib.QPARAMS_BYTES, dtype=torch.uint8, device="cuda")
+                    _lib.check(lib.axb_quantize_pad_range(x.data_ptr(), 1, 1, n, c, 0, 0, 0, 0, c, ordr.data_ptr(),
+                                                          int(mode == O.SIGNED), rounds[rname], p2.data_ptr(),
+                                                          codes.data_ptr(), None, fl.data_ptr(), s))
+                else:
+                    _lib.check(lib.axb_quantize_pad(x.data_ptr(), 1, 1, n, c, 0, 0, 0, 0, c, prm.data_ptr(),
+                                                    int(mode == O.SIGNED), rounds[rname], codes.data_ptr(), None,
+                                                    fl.data_ptr(), s))
+                got = codes.cpu().numpy().view(np.int8 if mode == O.SIGNED else np.uint8)
+                assert np.array_equal(got, want), (trial, c, dev_range, np.flatnonzero(got != want)[:5])
+                assert int(fl.item()) == 0
+    # non-finite input -> FLAG_NONFINITE
+    for bad in (np.nan, np.inf, -np.inf):
+        v = rng.standard_normal(4096 * 16).astype(np.float32)
+        v[777] = bad
+        x = torch.from_numpy(v.reshape(1, 1, 4096, 16)).cuda()
+        codes = torch.empty(v.size, dtype=torch.uint8, device="cuda")
+        fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(lib.axb_quantize_pad(x.data_ptr(), 1, 1, 4096, 16, 0, 0, 0, 0, 16, prm.data_ptr(), 1, 1,
+                                        codes.data_ptr(), None, fl.data_ptr(), s))
+        assert int(fl.item()) & _lib.FLAG_NONFINITE, bad
