@@ -606,7 +606,9 @@ def roofline_block(args, res, sm_count, max_mhz, sampled, total_ms):
 
 def hbm_block(args, res, peak_gbs):
     """GB/s of the memory-bound kernels (range, record decode, quantize, pools, add) from the eager
-    pass: algorithmic bytes (4 B per fp32 element read / written, 1 B per code) / event-timed launch."""
+    pass: algorithmic bytes (4 B per fp32 element read / written, 1 B per code) / event-timed launch;
+    for the quantizer also the committed ncu launch-list durations of the same kernels (no event
+    overhead; profiles/quantize_ncu_<workload>.json)."""
     agg: dict = {}
     # the depthwise conv does 9 lookups per output: it is memory-bound too (codes in, fp32 out)
     dw = [(nid, k, a, b, ab) for nid, a, b, _, ab, k in res["extra"]["profile"] if k.startswith("depthwise")]
@@ -624,6 +626,17 @@ def hbm_block(args, res, peak_gbs):
                              "frac": round(gbs / peak_gbs, 4) if peak_gbs else None}
         tb += nb
         tm += ms
+    qf = ROOT / "profiles" / f"quantize_ncu_{args.workload}.json"  # same kernels' ncu launch-list durations
+    if "quantize" in out["kernels"] and qf.exists():
+        try:
+            qn = json.loads(qf.read_text())
+            q = out["kernels"]["quantize"]
+            gbs = q["bytes_per_step"] / (qn["ms_per_step"] / 1e3) / 1e9
+            q["ncu_launch_list"] = {"ms_per_step": qn["ms_per_step"], "gbs": round(gbs, 1),
+                                    "frac": round(gbs / peak_gbs, 4) if peak_gbs else None,
+                                    "basis": qn["source"]}
+        except Exception:
+            pass
     out["all"] = {"gbs": round(tb / (tm / 1e3) / 1e9, 1) if tm else None,
                   "frac": round(tb / (tm / 1e3) / 1e9 / peak_gbs, 4) if tm and peak_gbs else None,
                   "share_of_step": round(tm / res["total_ms"], 4) if res["total_ms"] else None}
