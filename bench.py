@@ -646,8 +646,10 @@ def hbm_block(args, res, peak_gbs):
 def parity_block(args, spec, batch, y_rank0) -> dict:
     """Rank 0's logits vs the real reference's for the same batch (tests/golden/bench.npz)."""
     path = ROOT / "tests" / "golden" / "bench.npz"
-    key = f"{args.workload}_logits_sha"
-    if batch != spec["batch"] or (args.lut != "trunc2" and not spec.get("sweep")) or not path.exists():
+    # goldens: <workload>_* for truncated_lut(signed, 2) (and the sweep), <workload>exact_* for exact_lut
+    tag = args.workload if args.lut == "trunc2" or spec.get("sweep") else f"{args.workload}{args.lut}"
+    key = f"{tag}_logits_sha"
+    if batch != spec["batch"] or args.lut == "random" or not path.exists():
         return {"status": "unchecked", "why": "no reference golden for this workload / batch / table"}
     g = np.load(path)
     if key not in g:
@@ -655,9 +657,9 @@ def parity_block(args, spec, batch, y_rank0) -> dict:
     got = np.ascontiguousarray(y_rank0.reshape(batch, 1, 1, -1).astype(np.float32))
     sha = hashlib.sha256(got.tobytes()).digest()
     am = got.reshape(batch, -1).argmax(1)
-    ok = sha == g[key].tobytes() and np.array_equal(am, g[f"{args.workload}_argmax"])
+    ok = sha == g[key].tobytes() and np.array_equal(am, g[f"{tag}_argmax"])
     what = ("the sweep's first candidate network (truncated_lut(signed, 0))" if spec.get("sweep") else
-            "the same batch, weights and table")
+            f"the same batch, weights and table ({spec['lut']})")
     return {"status": "bit-exact" if ok else "MISMATCH",
             "against": f"tests/golden/bench.npz {key}: sha256 of all {batch} logits rows from the real reference "
                        f"graph.run (engine gemm) on {what}",

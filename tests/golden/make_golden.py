@@ -304,7 +304,8 @@ def make_bench() -> dict:
 
     lut = T.truncated_lut(T.Signedness.SIGNED, 2)
     out = {}
-    which = [a for a in sys.argv[1:] if a in ("r8", "r50", "mbv1", "r62sweep")] or ["r8", "r50", "mbv1", "r62sweep"]
+    which = ([a for a in sys.argv[1:] if a in ("r8", "r50", "mbv1", "r62sweep", "r50exact")]
+             or ["r8", "r50", "mbv1", "r62sweep", "r50exact"])
     path = HERE / "bench.npz"
     if path.exists():
         out.update(dict(np.load(path)))
@@ -314,6 +315,18 @@ def make_bench() -> dict:
     if "r50" in which:
         x, _ = datasets.synthetic_imagenet(256, seed=BENCH_SEED)
         run_reference("r50", resnet.resnet50(lut, seed=0), x, out)
+    if "r50exact" in which:
+        # config 5 control: the same ResNet-50 b256 with exact_lut(signed) (bench.py --lut exact); logits
+        # sha256 + argmax only
+        x, _ = datasets.synthetic_imagenet(256, seed=BENCH_SEED)
+        nodes = resnet.resnet50(T.exact_lut(T.Signedness.SIGNED), seed=0)
+        for n in nodes:
+            if "filters" in n["attrs"]:
+                n["attrs"]["filters"] = np.ascontiguousarray(n["attrs"]["filters"], np.float32)
+        y = axemu.run(to_reference_graph(nodes), Tensor4(x, Layout.NHWC), "gemm").data
+        out["r50exact_logits_sha"] = np.frombuffer(bytes.fromhex(sha(y)), np.uint8)
+        out["r50exact_argmax"] = y.reshape(256, -1).argmax(1)
+        print("r50exact argmax distinct", len(set(out["r50exact_argmax"].tolist())), flush=True)
     if "mbv1" in which:
         x, _ = datasets.synthetic_imagenet(256, seed=BENCH_SEED)
         run_reference("mbv1", resnet.mobilenet_v1(lut, seed=0), x, out)

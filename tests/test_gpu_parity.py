@@ -409,6 +409,23 @@ def test_sweep_first_candidate_full_batch_vs_reference():
     assert np.array_equal(y.reshape(1000, -1).argmax(1).cpu().numpy(), g["r62sweep_argmax"])
 
 
+def test_r50_exact_lut_full_batch_vs_reference():
+    """Config 5 control at the ResNet-50 shape: the benchmarked ResNet-50 b256 with exact_lut(signed)
+    (bench.py --lut exact) -- all 256 logits rows and the argmax bit-identical to the real reference's
+    graph.run on the same batch and weights (tests/golden/bench.npz r50exact_*)."""
+    torch = _torch()
+    from paper_2002_09481_b200 import datasets, resnet
+    from paper_2002_09481_b200 import types as T
+    from paper_2002_09481_b200.graph import GpuGraph
+
+    g = load_golden("bench")
+    assert "r50exact_logits_sha" in g
+    x = datasets.synthetic_imagenet(256, seed=1000)[0]
+    y = GpuGraph(resnet.resnet50(T.exact_lut(T.Signedness.SIGNED), seed=0)).run(torch.from_numpy(x).cuda())
+    assert _sha(y) == g["r50exact_logits_sha"].tobytes()
+    assert np.array_equal(y.reshape(256, -1).argmax(1).cpu().numpy(), g["r50exact_argmax"])
+
+
 def test_r50_full_batch_grid_invariant():
     """ResNet-50 at 256 images on a 100-SM persistent grid (other tile-to-CTA assignment) gives the
     reference's bits (the grid size must never change results)."""
