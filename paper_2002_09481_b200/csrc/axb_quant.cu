@@ -511,9 +511,12 @@ __global__ void __launch_bounds__(QT_H *QT_W) quantize_im2col_kernel(
     const int32_t *d_range,
     int is_signed, int round_mode, uint8_t *__restrict__ rows, int32_t *__restrict__ rowsum, int32_t *d_flags) {
     __shared__ QuantCtx q;
-    __shared__ uint8_t patch[kQiPatchMax];
+    __shared__ __align__(16) uint8_t patch[kQiPatchMax + 16];  // + a word of slack for the funnel reads
     pdl_launch_dependents();
     __shared__ int16_t koff[kMaxIm2colK];  // patch offset of window element k = (ky, kx, ci)
+    // koffw[wd]: patch offset of window byte 4*wd when bytes 4wd..4wd+3 are contiguous in the patch (one
+    // ky row's kx*c run, dilation 1 along x), else -1 (byte-by-byte gather)
+    __shared__ int16_t koffw[kMaxIm2colK / 4];
     if (d_range)
         quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
     else
@@ -526,6 +529,13 @@ __global__ void __launch_bounds__(QT_H *QT_W) quantize_im2col_kernel(
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
         const int t = k / c, ci = k - t * c;
         koff[k] = (int16_t)((t / kw) * dh * prow + (t % kw) * dw * c + ci);
+    }
+    __syncthreads();
+    for (int wd = threadIdx.x; wd < kp / 4; wd += blockDim.x) {
+        const int k0 = 4 * wd;
+        bool run = k0 + 3 < K;
+        for (int u = 1; run && u < 4; ++u) run = koff[k0 + u] == koff[k0] + u;
+        koffw[wd] = run ? koff[k0] : (int16_t)-1;
     }
     int nonfinite = 0;
     const int tid = threadIdx.x;
@@ -574,18 +584,26 @@ __global__ void __launch_bounds__(QT_H *QT_W) quantize_im2col_kernel(
         const int ty = tid / QT_W, tx = tid % QT_W;
         const int oy = oy0 + ty, ox = ox0 + tx;
         if (oy < oh && ox < ow) {
-            const uint8_t *base = patch + (ty * sh) * prow + (tx * sw) * c;
+            const int boff = (ty * sh) * prow + (tx * sw) * c;
+            const uint8_t *base = patch + boff;
+            const uint32_t *pwords = reinterpret_cast<const uint32_t *>(patch);
             const int64_t r = ((int64_t)b * oh + oy) * ow + ox;
             int32_t ssum = 0;
             for (int g = 0; g < kp / 16; ++g) {
                 uint32_t wv[4];
 #pragma unroll
                 for (int v4 = 0; v4 < 4; ++v4) {
+                    const int o = koffw[g * 4 + v4];
                     uint32_t word = 0;
+                    if (o >= 0) {  // 4 contiguous patch bytes: two aligned words, one funnel shift
+                        const uint32_t a = (uint32_t)(boff + o);
+                        word = __funnelshift_r(pwords[a >> 2], pwords[(a >> 2) + 1], (a & 3u) * 8u);
+                    } else {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int k = g * 16 + v4 * 4 + u;
-                        if (k < K) word |= (uint32_t)base[koff[k]] << (8 * u);
+                        for (int u = 0; u < 4; ++u) {
+                            const int k = g * 16 + v4 * 4 + u;
+                            if (k < K) word |= (uint32_t)base[koff[k]] << (8 * u);
+                        }
                     }
                     wv[v4] = word;
                     ssum = is_signed ? __dp4a((int)word, 0x01010101, ssum)  // junk bytes are 0
