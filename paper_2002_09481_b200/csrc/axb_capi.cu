@@ -89,7 +89,9 @@ __global__ void maxpool_kernel(const float *__restrict__ x, int64_t n, int64_t h
 // Vectorised pools for c % 4 == 0: one thread per (output pixel, 4 channels), float4 loads and
 // stores, 32-bit magic-number index division (the scalar kernels above spend most of their time
 // in 64-bit div/mod).  Identical per-element arithmetic and order.
-template <bool MAX>
+// PB taps' loads in flight per batch: 9 for windows of <= 9 taps (ResNet's 3x3 max pool: 36 fewer live
+// registers than 16, more resident warps), 16 otherwise (global average pools)
+template <bool MAX, int PB = 16>
 __global__ void __launch_bounds__(256) pool4_kernel(const float4 *__restrict__ x, int h, int w, int c4, int ph,
                                                     int pw, int sh, int sw, int pt, int pl, int oh, int ow,
                                                     uint32_t total, FastDiv fd_c4, FastDiv fd_ow, FastDiv fd_oh,
@@ -110,7 +112,6 @@ __global__ void __launch_bounds__(256) pool4_kernel(const float4 *__restrict__ x
         // taps in sequential (ky, kx) order, PB at a time: the PB loads are issued before the
         // dependent fp32 chain consumes them (a global 8x8 pool has only n*c/4 threads, so memory-
         // level parallelism per thread is what bounds it); the arithmetic order is unchanged
-        constexpr int PB = 16;
         const int taps = ph * pw;
         int ky = 0, kx = 0;
         for (int t0 = 0; t0 < taps; t0 += PB) {
@@ -297,7 +298,8 @@ int axb_maxpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, in
         const uint32_t t4 = (uint32_t)(total / 4);
         int pg, pb;
         pool_launch_dims(t4, &pg, &pb);
-        pool4_kernel<true><<<pg, pb, 0, (cudaStream_t)stream>>>(
+        auto fn = ph * pw <= 9 ? pool4_kernel<true, 9> : pool4_kernel<true, 16>;
+        fn<<<pg, pb, 0, (cudaStream_t)stream>>>(
             reinterpret_cast<const float4 *>(d_x), (int)h, (int)w, (int)(c / 4), ph, pw, sh, sw, pt, pl, (int)oh,
             (int)ow, t4, make_fastdiv((uint32_t)(c / 4)), make_fastdiv((uint32_t)ow), make_fastdiv((uint32_t)oh),
             reinterpret_cast<float4 *>(d_out), d_out_range, d_flags);
@@ -318,7 +320,8 @@ int axb_avgpool(const float *d_x, int64_t n, int64_t h, int64_t w, int64_t c, in
         const uint32_t t4 = (uint32_t)(total / 4);
         int pg, pb;
         pool_launch_dims(t4, &pg, &pb);
-        pool4_kernel<false><<<pg, pb, 0, (cudaStream_t)stream>>>(
+        auto fn = ph * pw <= 9 ? pool4_kernel<false, 9> : pool4_kernel<false, 16>;
+        fn<<<pg, pb, 0, (cudaStream_t)stream>>>(
             reinterpret_cast<const float4 *>(d_x), (int)h, (int)w, (int)(c / 4), ph, pw, sh, sw, pt, pl, (int)oh,
             (int)ow, t4, make_fastdiv((uint32_t)(c / 4)), make_fastdiv((uint32_t)ow), make_fastdiv((uint32_t)oh),
             reinterpret_cast<float4 *>(d_out), d_out_range, d_flags);
