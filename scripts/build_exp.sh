@@ -9,7 +9,7 @@ O=build/exp_$T; mkdir -p $O
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -warn-spills -Iinclude $*"
 for s in paper_2002_09481_b200/csrc/*.cu; do
   b=$(basename $s .cu)
-  if [ "$b" = axb_ftconv ] || [ "$b" = axb_depthwise ] || [ ! -f build/$b.o ]; then nvcc $F -c -o $O/$b.o $s & else cp build/$b.o $O/$b.o; fi
+  if [ "$b" = axb_ftconv ] || [ "$b" = axb_depthwise ] || [ "$b" = axb_quant ] || [ ! -f build/$b.o ]; then nvcc $F -c -o $O/$b.o $s & else cp build/$b.o $O/$b.o; fi
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $O/libaxb.so $O/*.o
