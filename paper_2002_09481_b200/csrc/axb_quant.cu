@@ -399,6 +399,76 @@ __global__ void __launch_bounds__(256) quantize_pad16_kernel(const float *__rest
     range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
 }
 
+// Unpadded inputs with no per-pixel sums (the CX / ftable kernels sum codes themselves): the code tensor
+// is the input tensor element for element (cs == c), so the pass is a flat stream.  A warp takes 512
+// consecutive floats per unit -- lane L loads float4 v*32 + L (v = 0..3), every load instruction one
+// contiguous 512-byte span, every code store one contiguous 128-byte span -- with the per-element
+// arithmetic of quantize_pad16_kernel (fast round-to-nearest, exact path near ties / non-finite).
+__global__ void __launch_bounds__(256) quantize_flat_kernel(const float *__restrict__ x, uint32_t nf4,
+                                                            axb_qparams *prm, const int32_t *d_range, int is_signed,
+                                                            int round_mode, uint32_t *__restrict__ codes,
+                                                            int32_t *d_flags) {
+    __shared__ QuantCtx q;
+    pdl_launch_dependents();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nunits = (nf4 + 127) >> 7;
+    const float4 *x4 = reinterpret_cast<const float4 *>(x);
+    float e[16];
+    auto fetch = [&](uint32_t uu) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint32_t idx = (uu << 7) + v * 32 + lane;
+            const float4 f = idx < nf4 ? __ldg(x4 + idx) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            e[4 * v] = f.x; e[4 * v + 1] = f.y; e[4 * v + 2] = f.z; e[4 * v + 3] = f.w;
+        }
+    };
+    uint32_t u = warp;
+    if (u < nunits) fetch(u);  // in flight during the coefficient prologue
+    if (d_range)
+        quant_ctx_from_range(q, d_range, is_signed, round_mode, prm);
+    else
+        quant_ctx_load(q, prm, is_signed);
+    const bool nearest = round_mode != AXB_ROUND_TOWARD_ZERO;
+    const float inv = q.inv, zpo = q.zpo;
+    const uint32_t flip = is_signed ? 0x80808080u : 0u;
+    int nonfinite = 0;
+    for (; u < nunits; u += nwarps) {
+        float uf[16];
+        bool ok = nearest;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            uf[k] = fmaf(e[k], inv, zpo);
+            ok &= fabsf(uf[k] - rintf(uf[k])) < 0.49975f;
+        }
+        uint32_t wv[4];
+        if (__builtin_expect(ok, 1)) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) wv[v] = pack_u8x4(uf[4 * v], uf[4 * v + 1], uf[4 * v + 2], uf[4 * v + 3]);
+        } else {
+            int uu[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                nonfinite |= !(fabsf(e[k]) <= 3.402823466e38f);
+                uu[k] = quant_any_u(q, e[k], nearest);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                wv[v] = (uint32_t)uu[4 * v] | ((uint32_t)uu[4 * v + 1] << 8) | ((uint32_t)uu[4 * v + 2] << 16) |
+                        ((uint32_t)uu[4 * v + 3] << 24);
+        }
+        const uint32_t base = u << 7;
+        if (u + nwarps < nunits) fetch(u + nwarps);  // the next unit's loads overlap these stores
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint32_t idx = base + v * 32 + lane;
+            if (idx < nf4) codes[idx] = wv[v] ^ flip;  // raw byte of code lo+u = (u + lo) & 0xFF
+        }
+    }
+    range_commit(INT32_MAX, INT32_MIN, nonfinite, nullptr, d_flags, AXB_FLAG_NONFINITE);
+}
+
 // ---------------------------------------------------------------- filters
 // HWCN fp32 -> (kpad, coutp) uint8 raw code bytes; row k = (ky*kw + kx)*cs + ci.
 __global__ void filters_codes_kernel(const float *__restrict__ f, int64_t kh, int64_t kw, int64_t c, int64_t cout,
@@ -763,6 +833,19 @@ static int quantize_pad_launch(const float *d_x, int64_t n, int64_t h, int64_t w
     if (total * (cs / 4) >= (int64_t(1) << 31)) return set_error(AXB_E_VALUE, "quantize: more than 2^31 code words");
     const FastDiv fhp = make_fastdiv((uint32_t)hp), fwp = make_fastdiv((uint32_t)wp);
     const int64_t c16 = c / 16;
+#ifndef AXB_EXP_NO_FLAT
+    if (pt == 0 && pb == 0 && pl == 0 && pr == 0 && d_pixsum == nullptr && c % 16 == 0 && cs == c &&
+        (reinterpret_cast<uintptr_t>(d_x) & 15) == 0) {
+        // unpadded, no pixel sums: the flat stream kernel (one resident wave)
+        const int64_t nf4 = total * c / 4;
+        int64_t blocks = (nf4 / 128 + 8) / 8;  // 8 warps per CTA, one 128-float4 unit per warp
+        const int64_t capf = (int64_t)sm_count() * 4;
+        if (blocks > capf) blocks = capf;
+        quantize_flat_kernel<<<(int)blocks, 256, 0, s>>>(d_x, (uint32_t)nf4, d_params, d_range, is_signed, round_mode,
+                                                        reinterpret_cast<uint32_t *>(d_codes), d_flags);
+        return check_launch("quantize_flat");
+    }
+#endif
     if (c % 16 == 0 && c16 <= 128 && (c16 & (c16 - 1)) == 0 && ((reinterpret_cast<uintptr_t>(d_x) & 15) == 0)) {
         // wide pixels (c = 1024, 2048): one warp per 32 chunks, per-pixel sums by atomics into a zeroed buffer
         if (c16 > 32 && d_pixsum && cudaMemsetAsync(d_pixsum, 0, total * 4, s) != cudaSuccess)
